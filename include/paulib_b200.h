@@ -1,0 +1,177 @@
+/*
+ * paulib_b200 — C ABI of the B200-native Pauli-sum hot path.
+ *
+ * Plain pointers and sizes only (no torch types).  Every pointer argument
+ * except `plan`, `out_count_host` and the *_bytes queries is a DEVICE pointer;
+ * `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ * Functions return PL_OK (0) or a negative PL_ERR_* code; pl_last_error()
+ * returns a thread-local message for the last failure.
+ *
+ * Storage (the reference's PauliSumSoA, sums.py:429-450): for a sum of M
+ * terms at W = tier/64 words per plane (bits.py:12, :34-46)
+ *   x, z : W planes, word w of term t at plane[w * ld + t] (ld >= M)
+ *   k    : M uint8 phase exponents (factor i^k)
+ *   c    : M complex128 coefficients, interleaved (re, im) doubles
+ * The reference's (M, W) "columns" are the transpose of these planes
+ * (sums.py:459-460).
+ *
+ * Each entry point names the reference interface it replaces (file:line in
+ * /root/reference/pkg/src/paulialg/).
+ */
+#ifndef PAULIB_B200_H
+#define PAULIB_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PL_OK 0
+#define PL_ERR_ARG (-1)       /* bad size / pointer / alignment            */
+#define PL_ERR_TIER (-2)      /* W not in {1,2,4,8,16}  (bits.py CapacityError) */
+#define PL_ERR_CUDA (-3)      /* CUDA runtime error                         */
+#define PL_ERR_CAPACITY (-4)  /* problem larger than the documented limits  */
+#define PL_ERR_WORKSPACE (-5) /* workspace smaller than the plan requires   */
+
+#define PL_ABI_VERSION 1
+
+/* Thread-local description of the most recent error. */
+const char* pl_last_error(void);
+int pl_abi_version(void);
+
+/* ------------------------------------------------------------------------
+ * K1 — batched pair multiply.  Replaces bench.py:168-177 (_batch_pair_multiply)
+ * and the per-pair math of strings.py:32-44 (_phase_exponent_words) and
+ * strings.py:133-137 (PauliString.multiply):
+ *   o.x = a.x ^ b.x,  o.z = a.z ^ b.z,
+ *   o.k = (a.k + b.k + phase(a, b)) mod 4,
+ * for P aligned pairs.  Planes use leading dimensions lda/ldb/ldo (words).
+ * ak / bk may be NULL (treated as 0).
+ */
+int pl_batch_multiply(int W, int64_t P,
+                      const uint64_t* ax, const uint64_t* az, const uint8_t* ak, int64_t lda,
+                      const uint64_t* bx, const uint64_t* bz, const uint8_t* bk, int64_t ldb,
+                      uint64_t* ox, uint64_t* oz, uint8_t* ok, int64_t ldo,
+                      void* stream);
+
+/* Batched symplectic inner product parity (strings.py:47-51, :141-147):
+ * anti[p] = 1 when pair p anti-commutes, 0 when it commutes. */
+int pl_batch_sip(int W, int64_t P,
+                 const uint64_t* ax, const uint64_t* az, int64_t lda,
+                 const uint64_t* bx, const uint64_t* bz, int64_t ldb,
+                 uint8_t* anti, void* stream);
+
+/* ------------------------------------------------------------------------
+ * K2 raw — outer product without combine.  Replaces sums.py:144-174
+ * (_multiply_columns) + sums.py:123-141 (_multiply_block): output row
+ * j*Ma + i holds a_i * b_j (j-major), phase exponent
+ * (a.k[i] + b.k[j] + phase(a_i, b_j)) mod 4 and coefficient a.c[i] * b.c[j]
+ * (IEEE products, no fused multiply-add).  Output planes have Ma*Mb columns.
+ */
+int pl_outer_multiply_raw(int W, int64_t Ma, int64_t Mb,
+                          const uint64_t* ax, const uint64_t* az, const uint8_t* ak,
+                          const double* ac, int64_t lda,
+                          const uint64_t* bx, const uint64_t* bz, const uint8_t* bk,
+                          const double* bc, int64_t ldb,
+                          uint64_t* ox, uint64_t* oz, uint8_t* ok, double* oc, int64_t ldo,
+                          void* stream);
+
+/* ------------------------------------------------------------------------
+ * K2-K4 — multiply + simplify.  A merge "plan" fixes the packed-key layout
+ * (bit ranges of the (z0..z{W-1}, x0..x{W-1}) canonical key that can be
+ * nonzero, sums.py:104-106 / strings.py:165-167), the bucket count and the
+ * workspace size.  pl_*_plan() reads device data and SYNCHRONISES `stream`.
+ */
+#define PL_PLAN_MAX_SEG 32
+
+typedef struct pl_merge_plan {
+  int32_t W;             /* words per plane                                  */
+  int32_t mode;          /* 0 = outer product A*B, 1 = sort_and_combine(S)   */
+  int64_t ma, mb;        /* outer: |A|, |B|; sort: M, 1                      */
+  int64_t n_items;       /* raw terms to merge (ma*mb, or M)                 */
+  int32_t key_words;     /* KW: 64-bit words per packed key                  */
+  int32_t key_bits;      /* packed key length in bits                        */
+  int32_t seg_lo[PL_PLAN_MAX_SEG];  /* per canonical-key word: lowest used bit */
+  int32_t seg_len[PL_PLAN_MAX_SEG]; /* number of bits kept (0 = word unused)  */
+  int32_t seg_pos[PL_PLAN_MAX_SEG]; /* offset of the segment in the key (MSB first) */
+  int32_t n_buckets;     /* level-1 buckets (splitter ranges)                */
+  int32_t n_samples;     /* splitter sample size                             */
+  int32_t leaf_cap;      /* largest bucket sorted in shared memory           */
+  int32_t leaf_target;   /* target size of a level-2 sub-bucket              */
+  int32_t max_sub;       /* max sub-buckets per level-1 bucket               */
+  int32_t pad0;
+  int64_t workspace_bytes;
+  int64_t reserved[8];
+} pl_merge_plan;
+
+/* Plan for A*B (sums.py:293-305).  Requires Ma*Mb <= 2^30. */
+int pl_outer_plan(int W, int64_t Ma, int64_t Mb,
+                  const uint64_t* ax, const uint64_t* az, int64_t lda,
+                  const uint64_t* bx, const uint64_t* bz, int64_t ldb,
+                  pl_merge_plan* plan, void* stream);
+
+/* Plan for sort_and_combine of M terms (sums.py:286-291).  M <= 2^30. */
+int pl_sort_plan(int W, int64_t M, const uint64_t* x, const uint64_t* z, int64_t ld,
+                 pl_merge_plan* plan, void* stream);
+
+/* Outer product followed by _combine_columns (sums.py:94-120): fold i^k into
+ * the coefficient, order by the canonical key, merge equal keys (summing in
+ * raw-row order), drop |c| <= eps, flags 0.  Output planes need capacity
+ * >= plan->n_items columns (ldo); *out_count (device int64) receives the
+ * number of merged terms.  Deterministic: bit-identical run to run. */
+int pl_outer_multiply_combine(const pl_merge_plan* plan,
+                              const uint64_t* ax, const uint64_t* az, const uint8_t* ak,
+                              const double* ac, int64_t lda,
+                              const uint64_t* bx, const uint64_t* bz, const uint8_t* bk,
+                              const double* bc, int64_t ldb,
+                              double eps, void* workspace, size_t workspace_bytes,
+                              uint64_t* ox, uint64_t* oz, uint8_t* ok, double* oc, int64_t ldo,
+                              int64_t* out_count, void* stream);
+
+/* sort_and_combine (sums.py:286-291 / :94-120) of one sum. */
+int pl_sort_combine(const pl_merge_plan* plan,
+                    const uint64_t* x, const uint64_t* z, const uint8_t* k, const double* c,
+                    int64_t ld, double eps, void* workspace, size_t workspace_bytes,
+                    uint64_t* ox, uint64_t* oz, uint8_t* ok, double* oc, int64_t ldo,
+                    int64_t* out_count, void* stream);
+
+/* ------------------------------------------------------------------------
+ * K5 — commutation bitmatrix.  Restates the all-pairs block of
+ * grouping.py:136-140 (parity of popc(x_r & z_c) + popc(z_r & x_c)):
+ * bit (c - col0) % 32 of word bits[(r - row0) * ld_bits + (c - col0) / 32]
+ * is 1 when term r anti-commutes with term c, for r in [row0, row0+rows),
+ * c in [col0, col0+cols).  Rows and columns index the same M-term sum.
+ * col0 must be a multiple of 32; trailing bits of the last word are 0.
+ * method: 0 = auto, 1 = row-list XOR over transposed column slices
+ * (sparse-friendly), 2 = direct LOP3/POPC per pair.
+ */
+int pl_commutation_bitmatrix(int W, int64_t M,
+                             const uint64_t* x, const uint64_t* z, int64_t ld,
+                             int64_t row0, int64_t rows, int64_t col0, int64_t cols,
+                             uint32_t* bits, int64_t ld_bits, int method,
+                             void* workspace, size_t workspace_bytes, void* stream);
+
+/* Workspace bytes pl_commutation_bitmatrix needs for `rows` rows. */
+int64_t pl_bitmatrix_workspace_bytes(int W, int64_t rows);
+
+/* ------------------------------------------------------------------------
+ * K6 — greedy first-fit commutation grouping.  Replaces grouping.py:67-95
+ * (_greedy_over / group_greedy): term t (index order) joins the first group
+ * (creation order) all of whose members commute with it, else opens a new
+ * group.  group_of[t] receives t's group id (ids in creation order);
+ * *n_groups the group count; *pair_checks the reference's
+ * GroupingStats.pair_checks (grouping.py:75-76).  All three are device
+ * pointers.  Deterministic and exactly equal to the reference.
+ */
+int64_t pl_group_workspace_bytes(int W, int64_t M);
+int pl_group_greedy(int W, int64_t M, const uint64_t* x, const uint64_t* z, int64_t ld,
+                    int32_t* group_of, int32_t* n_groups, int64_t* pair_checks,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PAULIB_B200_H */

@@ -1,0 +1,136 @@
+"""Greedy first-fit commutation grouping (K6) behind the reference API.
+
+Mirrors ``paulialg/grouping.py``: :class:`GroupingStats` (:22-26),
+:class:`CommutationPartition` (:29-48), :class:`ValidationReport` (:51-57),
+:func:`group_greedy` (:91-95), :func:`validate_partition` (:149-181).  The
+assignment is computed on the GPU by ``pl_group_greedy`` and is identical to
+the reference's sequential first-fit scan (:67-83), including the
+``pair_checks`` counter (:75-76).  ``group_greedy_parallel`` (the two-phase
+chunked variant, :98-146) is outside this build's hot-path scope.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from ._device import ptr, stream_ptr
+from .sums import PauliSumSoA, _compute_device
+
+
+@dataclass
+class GroupingStats:
+    """Number of pairwise commutation checks performed (grouping.py:22-26)."""
+
+    pair_checks: int = 0
+
+
+@dataclass
+class CommutationPartition:
+    """Ordered groups of term indices (grouping.py:29-48)."""
+
+    groups: list[list[int]]
+    source_size: int
+
+    def group_count(self) -> int:
+        return len(self.groups)
+
+    def to_text(self) -> str:
+        return "".join(" ".join(str(i) for i in g) + "\n" for g in self.groups)
+
+    @classmethod
+    def from_text(cls, text: str, source_size: int | None = None) -> "CommutationPartition":
+        groups = [[int(t) for t in line.split()] for line in text.splitlines() if line.strip()]
+        if source_size is None:
+            source_size = sum(len(g) for g in groups)
+        return cls(groups, source_size)
+
+    @classmethod
+    def from_assignment(cls, group_of: np.ndarray) -> "CommutationPartition":
+        """Groups in id order, members ascending, from a per-term group id array."""
+        g = np.asarray(group_of, dtype=np.int64)
+        m = g.shape[0]
+        if m == 0:
+            return cls([], 0)
+        order = np.argsort(g, kind="stable")
+        bounds = np.flatnonzero(np.diff(g[order])) + 1
+        groups = [part.tolist() for part in np.split(order, bounds)]
+        return cls(groups, m)
+
+
+@dataclass
+class ValidationReport:
+    ok: bool
+    message: str = ""
+    violation: tuple[int, int] | None = None
+
+
+def group_assignment(s: PauliSumSoA):
+    """Device call: (group_of (M,) int32, n_groups, pair_checks) on the GPU."""
+    if not isinstance(s, PauliSumSoA):
+        s = s.to_soa()
+    dev, _ = _compute_device(s)
+    S = s.to(dev).planes()
+    M = S.M
+    gof = torch.empty(max(M, 1), dtype=torch.int32, device=dev)
+    ng = torch.zeros(1, dtype=torch.int32, device=dev)
+    pc = torch.zeros(1, dtype=torch.int64, device=dev)
+    if M:
+        ws_bytes = int(_native.load().pl_group_workspace_bytes(S.W, M))
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+        with torch.cuda.device(dev):
+            _native.call("pl_group_greedy", S.W, M, ptr(S.x), ptr(S.z), S.ld, ptr(gof), ptr(ng),
+                         ptr(pc), ptr(ws), ws.numel(), stream_ptr(dev))
+    return gof[:M], ng, pc
+
+
+def group_greedy(s, *, stats: GroupingStats | None = None) -> CommutationPartition:
+    """Deterministic first-fit grouping (grouping.py:91-95)."""
+    gof, _, pc = group_assignment(s)
+    part = CommutationPartition.from_assignment(gof.cpu().numpy())
+    if stats is not None:
+        stats.pair_checks += int(pc.item())
+    return part
+
+
+def validate_partition(s, p: CommutationPartition) -> ValidationReport:
+    """Disjoint, complete, pairwise commuting (grouping.py:149-181).
+
+    Pairwise commutation of every group is checked on the GPU with the
+    commutation bitmatrix restricted to each group's members.
+    """
+    from .bitmatrix import commutation_bitmatrix, unpack_bits
+
+    if not isinstance(s, PauliSumSoA):
+        s = s.to_soa()
+    m = len(s)
+    if p.source_size != m:
+        return ValidationReport(False, f"partition built for {p.source_size} terms, sum has {m}")
+    seen = np.zeros(m, dtype=bool)
+    for gi, g in enumerate(p.groups):
+        for t in g:
+            if not 0 <= t < m:
+                return ValidationReport(False, f"group {gi} references term {t} out of range")
+            if seen[t]:
+                return ValidationReport(False, f"term {t} appears in more than one group")
+            seen[t] = True
+    if not seen.all():
+        return ValidationReport(False, f"term {int(np.flatnonzero(~seen)[0])} missing from the partition")
+    dev, _ = _compute_device(s)
+    sd = s.to(dev)
+    for gi, g in enumerate(p.groups):
+        if len(g) < 2:
+            continue
+        idx = torch.as_tensor(g, dtype=torch.int64, device=dev)
+        sub = PauliSumSoA(s.n, sd.x[:, idx], sd.z[:, idx], sd.flags[idx], sd.coeffs[idx],
+                          validate=False)
+        bits = unpack_bits(commutation_bitmatrix(sub), len(g)).cpu().numpy()
+        bad = np.argwhere(np.triu(bits, 1))
+        if bad.size:
+            a, b = int(bad[0, 0]), int(bad[0, 1])
+            return ValidationReport(False, f"terms {g[a]} and {g[b]} in group {gi} anti-commute",
+                                    violation=(g[a], g[b]))
+    return ValidationReport(True, "partition valid")

@@ -1,0 +1,518 @@
+"""Weighted Pauli sums: device-resident SoA planes (the hot-path storage) and the
+reference's packed AoS records, behind the reference's public API.
+
+Mirrors ``paulialg/sums.py``:
+
+* :class:`PauliSumSoA` — the north-star layout (sums.py:429-477): x, z as
+  (W, M) uint64 planes, a phase byte and a complex128 coefficient per term.
+  Here the planes are torch tensors, normally on a CUDA device; a sum whose
+  tensors live on the host is uploaded for every operation and its results
+  come back to the host (the end-to-end path).
+* :class:`PauliSum` — the packed array-of-structures record
+  ``x[W] u64, z[W] u64, flags u8, coeff c128`` (sums.py:48-57, :360-426),
+  kept on the host as a numpy structured array for drop-in compatibility;
+  operations transpose it to SoA planes on the device.
+* ``multiply`` (sums.py:293-305), ``sort_and_combine`` (sums.py:286-291),
+  ``sum_multiply`` / ``sort_and_combine`` module wrappers (sums.py:484-489).
+
+All arithmetic runs in the native CUDA kernels (no CPU fallback).  The
+``threads`` argument of ``multiply`` is accepted for signature compatibility;
+the GPU result is bit-identical for every value, as the reference guarantees
+for its thread split (sums.py:296-299).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Iterable, Iterator, Sequence, Union
+
+import numpy as np
+import torch
+
+from . import _native
+from ._device import (as_c128, as_u8, cuda_device, i64_tensor_to_u64, plane_ld, ptr, stream_ptr,
+                      u64_to_i64_tensor)
+from .bits import DimensionError, PHASE_FACTORS, tier_for
+from .strings import PauliString
+
+
+@dataclass(frozen=True)
+class PauliTerm:
+    """One (coefficient, string) entry of a sum (sums.py:31-42)."""
+
+    coeff: complex
+    string: PauliString
+
+    def __post_init__(self):
+        c = complex(self.coeff)
+        if not (math.isfinite(c.real) and math.isfinite(c.imag)):
+            raise ValueError(f"coefficient must be finite, got {c}")
+        object.__setattr__(self, "coeff", c)
+
+
+TermEntry = Union[PauliTerm, tuple]
+
+
+def aos_dtype(words: int) -> np.dtype:
+    """Packed record: x-words, z-words, flags byte, coefficient (sums.py:48-57)."""
+    return np.dtype([("x", np.uint64, (words,)), ("z", np.uint64, (words,)),
+                     ("flags", np.uint8), ("coeff", np.complex128)])
+
+
+def _entries_to_columns(entries: Sequence[TermEntry], n: int | None):
+    """(coeff, label-or-string) entries -> (n, x (M,W), z, flags, coeffs) (sums.py:60-91)."""
+    coeffs, strings = [], []
+    for e in entries:
+        c, s = (e.coeff, e.string) if isinstance(e, PauliTerm) else e
+        if not isinstance(s, PauliString):
+            s = PauliString.from_label(str(s))
+        c = complex(c)
+        if not (math.isfinite(c.real) and math.isfinite(c.imag)):
+            raise ValueError(f"coefficient must be finite, got {c}")
+        if n is None:
+            n = s.n
+        elif s.n != n:
+            raise DimensionError(f"term on {s.n} qubits in a {n}-qubit sum")
+        coeffs.append(c)
+        strings.append(s)
+    if n is None:
+        raise ValueError("qubit count required for an empty sum")
+    W = tier_for(n) // 64
+    m = len(strings)
+    x = np.zeros((m, W), np.uint64)
+    z = np.zeros((m, W), np.uint64)
+    flags = np.zeros(m, np.uint8)
+    for i, s in enumerate(strings):
+        x[i], z[i], flags[i] = s.x, s.z, s.phase
+    return n, x, z, flags, np.array(coeffs, dtype=np.complex128).reshape(m)
+
+
+def _check_finite_np(c: np.ndarray) -> None:
+    if c.size and not np.isfinite(c).all():
+        raise ValueError("coefficients must be finite")
+
+
+class _Planes:
+    """Device view of a sum: (W, M) int64 planes + flags + coeffs on one device."""
+
+    __slots__ = ("x", "z", "k", "c", "W", "M", "ld")
+
+    def __init__(self, x, z, k, c):
+        if plane_ld(x) != plane_ld(z):
+            x, z = x.contiguous(), z.contiguous()
+        self.x, self.z, self.k, self.c = x, z, k.contiguous(), c.contiguous()
+        self.W, self.M = x.shape
+        self.ld = plane_ld(x)
+
+
+class PauliSumSoA:
+    """Struct-of-arrays sum: word w of every term contiguous (sums.py:429-477).
+
+    ``x``/``z`` are (W, M) torch.int64 tensors holding uint64 bit patterns
+    (unit stride along M; the plane stride may exceed M), ``flags`` (M,)
+    uint8 and ``coeffs`` (M,) complex128, all on one device.
+    """
+
+    __slots__ = ("n", "tier", "x", "z", "flags", "coeffs")
+
+    def __init__(self, n, x, z, flags, coeffs, *, device=None, validate: bool = True):
+        self.n = int(n)
+        self.tier = tier_for(self.n)
+        W = self.tier // 64
+        if validate and not isinstance(coeffs, torch.Tensor):
+            _check_finite_np(np.asarray(coeffs, dtype=np.complex128))
+        xt, zt = u64_to_i64_tensor(x), u64_to_i64_tensor(z)
+        if xt.dim() != 2 or xt.shape[0] != W or zt.shape != xt.shape:
+            raise ValueError(f"expected ({W}, M) word arrays, got {tuple(xt.shape)} and "
+                             f"{tuple(zt.shape)}")
+        m = xt.shape[1]
+        ft, ct = as_u8(flags), as_c128(coeffs)
+        if ft.shape != (m,) or ct.shape != (m,):
+            raise ValueError("flags and coeffs must have one entry per term")
+        if device is not None:
+            dev = torch.device(device)
+            nb = dev.type == "cuda"
+            xt, zt = xt.to(dev, non_blocking=nb), zt.to(dev, non_blocking=nb)
+            ft, ct = ft.to(dev, non_blocking=nb), ct.to(dev, non_blocking=nb)
+        if validate and isinstance(coeffs, torch.Tensor) and ct.numel():
+            if not bool(torch.isfinite(torch.view_as_real(ct)).all()):
+                raise ValueError("coefficients must be finite")
+        self.x, self.z, self.flags, self.coeffs = xt, zt, ft, ct
+
+    # ----------------------------------------------------------- creation
+    @classmethod
+    def from_columns(cls, n, x, z, flags, coeffs, *, device=None, validate=True):
+        """From the reference's (M, W) column layout (sums.py:455-457)."""
+        x = np.asarray(x, dtype=np.uint64)
+        z = np.asarray(z, dtype=np.uint64)
+        W = tier_for(n) // 64
+        x = x.reshape(-1, W)
+        z = z.reshape(-1, W)
+        return cls(n, np.ascontiguousarray(x.T), np.ascontiguousarray(z.T), flags, coeffs,
+                   device=device, validate=validate)
+
+    _from_columns = from_columns
+
+    @classmethod
+    def from_terms(cls, entries: Iterable[TermEntry], n: int | None = None, *, device=None):
+        n, x, z, flags, coeffs = _entries_to_columns(list(entries), n)
+        return cls.from_columns(n, x, z, flags, coeffs, device=device)
+
+    @classmethod
+    def empty(cls, n: int, device=None):
+        W = tier_for(n) // 64
+        return cls(n, np.zeros((W, 0), np.uint64), np.zeros((W, 0), np.uint64),
+                   np.zeros(0, np.uint8), np.zeros(0, np.complex128), device=device)
+
+    # -------------------------------------------------------------- views
+    @property
+    def words(self) -> int:
+        return self.tier // 64
+
+    @property
+    def device(self) -> torch.device:
+        return self.x.device
+
+    def __len__(self) -> int:
+        return int(self.x.shape[1])
+
+    def to(self, device) -> "PauliSumSoA":
+        dev = torch.device(device)
+        if dev == self.device:
+            return self
+        nb = dev.type == "cuda"
+        out = object.__new__(PauliSumSoA)
+        out.n, out.tier = self.n, self.tier
+        out.x = self.x.to(dev, non_blocking=nb)
+        out.z = self.z.to(dev, non_blocking=nb)
+        out.flags = self.flags.to(dev, non_blocking=nb)
+        out.coeffs = self.coeffs.to(dev, non_blocking=nb)
+        return out
+
+    def cuda(self, device=None) -> "PauliSumSoA":
+        return self.to(cuda_device(device))
+
+    def cpu(self) -> "PauliSumSoA":
+        return self.to("cpu")
+
+    def columns(self):
+        """Host numpy (x (M,W), z (M,W), flags, coeffs) (sums.py:459-460)."""
+        x = i64_tensor_to_u64(self.x).T
+        z = i64_tensor_to_u64(self.z).T
+        return (x, z, self.flags.detach().cpu().numpy(), self.coeffs.detach().cpu().numpy())
+
+    _columns = columns
+
+    def planes(self) -> _Planes:
+        return _Planes(self.x, self.z, self.flags, self.coeffs)
+
+    @property
+    def payload_nbytes(self) -> int:
+        m = len(self)
+        return 2 * self.words * 8 * m + m + 16 * m
+
+    def term(self, i: int) -> PauliTerm:
+        x, z = i64_tensor_to_u64(self.x[:, i:i + 1])[:, 0], i64_tensor_to_u64(self.z[:, i:i + 1])[:, 0]
+        k = int(self.flags[i].item())
+        c = complex(self.coeffs[i].item())
+        return PauliTerm(c, PauliString(self.n, x.copy(), z.copy(), k, validate=False))
+
+    def __iter__(self) -> Iterator[PauliTerm]:
+        x, z, f, c = self.columns()
+        for i in range(len(self)):
+            yield PauliTerm(complex(c[i]), PauliString(self.n, x[i].copy(), z[i].copy(),
+                                                       int(f[i]), validate=False))
+
+    def labels(self) -> list[str]:
+        return [t.string.label for t in self]
+
+    def canonical_key(self, i: int) -> bytes:
+        """(z-words, x-words) big-endian key of term i (sums.py:277-280)."""
+        t = self.term(i).string
+        return t.canonical_key()
+
+    def __eq__(self, other) -> bool:
+        if type(other) is not type(self):
+            return NotImplemented
+        if self.n != other.n or len(self) != len(other):
+            return False
+        ax, az, af, ac = self.columns()
+        bx, bz, bf, bc = other.columns()
+        return (np.array_equal(ax, bx) and np.array_equal(az, bz) and np.array_equal(af, bf)
+                and np.array_equal(ac, bc))
+
+    __hash__ = None
+
+    def __repr__(self) -> str:
+        return f"PauliSumSoA(n={self.n}, terms={len(self)}, device={self.device})"
+
+    def to_aos(self) -> "PauliSum":
+        """Inverse of PauliSum.to_soa (sums.py:469-477)."""
+        return PauliSum.from_columns(self.n, *self.columns())
+
+    def _check_same_n(self, other) -> None:
+        if self.n != other.n:
+            raise DimensionError(f"qubit counts differ: {self.n} != {other.n}")
+
+    # ---------------------------------------------------------- operations
+    def multiply(self, other, *, threads: int = 1, eps: float = 0.0, combine: bool = True):
+        """Outer product; canonical unless combine=False (sums.py:293-305)."""
+        self._check_same_n(other)
+        other = other if isinstance(other, PauliSumSoA) else other.to_soa()
+        return outer_multiply(self, other, eps=eps, combine=combine)
+
+    __mul__ = multiply
+
+    def sort_and_combine(self, eps: float = 0.0):
+        """Canonical form: sorted, merged, |c| <= eps dropped (sums.py:286-291)."""
+        if eps < 0:
+            raise ValueError("eps must be >= 0")
+        return sort_combine(self, eps=eps)
+
+    def truncate(self, eps: float):
+        """Drop terms with |coeff| <= eps, keeping order (sums.py:327-339)."""
+        if eps < 0:
+            raise ValueError("eps must be >= 0")
+        keep = torch.abs(self.coeffs) > eps
+        out = object.__new__(PauliSumSoA)
+        out.n, out.tier = self.n, self.tier
+        out.x = self.x[:, keep].contiguous()
+        out.z = self.z[:, keep].contiguous()
+        out.flags = self.flags[keep].contiguous()
+        out.coeffs = self.coeffs[keep].contiguous()
+        return out
+
+
+class PauliSum:
+    """Array-of-structures sum on the host, packed records (sums.py:360-426)."""
+
+    __slots__ = ("n", "tier", "_data")
+
+    def __init__(self, n: int, data: np.ndarray | None = None):
+        self.n = int(n)
+        self.tier = tier_for(self.n)
+        dt = aos_dtype(self.tier // 64)
+        if data is None:
+            data = np.empty(0, dtype=dt)
+        if data.dtype != dt:
+            raise ValueError(f"expected dtype {dt}, got {data.dtype}")
+        _check_finite_np(data["coeff"])
+        self._data = data
+
+    @classmethod
+    def from_columns(cls, n, x, z, flags, coeffs):
+        _check_finite_np(np.asarray(coeffs))
+        out = cls(n)
+        x = np.asarray(x, dtype=np.uint64)
+        data = np.empty(x.shape[0], dtype=aos_dtype(tier_for(n) // 64))
+        data["x"], data["z"], data["flags"], data["coeff"] = x, z, flags, coeffs
+        out._data = data
+        return out
+
+    _from_columns = from_columns
+
+    @classmethod
+    def from_terms(cls, entries: Iterable[TermEntry], n: int | None = None):
+        return cls.from_columns(*_entries_to_columns(list(entries), n))
+
+    def columns(self):
+        d = self._data
+        return d["x"], d["z"], d["flags"], d["coeff"]
+
+    _columns = columns
+
+    @property
+    def words(self) -> int:
+        return self.tier // 64
+
+    def __len__(self) -> int:
+        return int(self._data.shape[0])
+
+    @property
+    def coeffs(self) -> np.ndarray:
+        return self._data["coeff"]
+
+    @property
+    def flags(self) -> np.ndarray:
+        return self._data["flags"]
+
+    @property
+    def x_matrix(self) -> np.ndarray:
+        return self._data["x"]
+
+    @property
+    def z_matrix(self) -> np.ndarray:
+        return self._data["z"]
+
+    @property
+    def payload_nbytes(self) -> int:
+        return self._data.nbytes
+
+    def term(self, i: int) -> PauliTerm:
+        d = self._data[i]
+        return PauliTerm(complex(d["coeff"]),
+                         PauliString(self.n, d["x"].copy(), d["z"].copy(), int(d["flags"]),
+                                     validate=False))
+
+    def __iter__(self):
+        return (self.term(i) for i in range(len(self)))
+
+    def labels(self) -> list[str]:
+        return [t.string.label for t in self]
+
+    def canonical_key(self, i: int) -> bytes:
+        return self.term(i).string.canonical_key()
+
+    def to_soa(self, device=None) -> PauliSumSoA:
+        """Transpose into SoA planes (sums.py:417-426); ``device`` optional."""
+        d = self._data
+        return PauliSumSoA(self.n, np.ascontiguousarray(d["x"].T), np.ascontiguousarray(d["z"].T),
+                           d["flags"].copy(), d["coeff"].copy(), device=device, validate=False)
+
+    def __eq__(self, other) -> bool:
+        if type(other) is not type(self):
+            return NotImplemented
+        return self.n == other.n and self._data.tobytes() == other._data.tobytes()
+
+    __hash__ = None
+
+    def __repr__(self) -> str:
+        return f"PauliSum(n={self.n}, terms={len(self)})"
+
+    def _check_same_n(self, other) -> None:
+        if self.n != other.n:
+            raise DimensionError(f"qubit counts differ: {self.n} != {other.n}")
+
+    def multiply(self, other, *, threads: int = 1, eps: float = 0.0, combine: bool = True):
+        self._check_same_n(other)
+        b = other.to_soa() if isinstance(other, PauliSum) else other
+        return self.to_soa().multiply(b, eps=eps, combine=combine).to_aos()
+
+    __mul__ = multiply
+
+    def sort_and_combine(self, eps: float = 0.0):
+        if eps < 0:
+            raise ValueError("eps must be >= 0")
+        return self.to_soa().sort_and_combine(eps).to_aos()
+
+    def truncate(self, eps: float):
+        if eps < 0:
+            raise ValueError("eps must be >= 0")
+        keep = np.abs(self._data["coeff"]) > eps
+        return PauliSum(self.n, self._data[keep].copy())
+
+
+# ----------------------------------------------------------- kernel drivers
+def _compute_device(*sums: PauliSumSoA) -> tuple[torch.device, bool]:
+    """The CUDA device to run on and whether results go back to the host."""
+    for s in sums:
+        if s.device.type == "cuda":
+            return s.device, False
+    return cuda_device(), True
+
+
+def _new_sum(n, x, z, k, c) -> PauliSumSoA:
+    out = object.__new__(PauliSumSoA)
+    out.n, out.tier = int(n), tier_for(n)
+    out.x, out.z, out.flags, out.coeffs = x, z, k, c
+    return out
+
+
+def _alloc_planes(W: int, cap: int, dev):
+    x = torch.empty((W, max(cap, 1)), dtype=torch.int64, device=dev)
+    z = torch.empty((W, max(cap, 1)), dtype=torch.int64, device=dev)
+    k = torch.empty(max(cap, 1), dtype=torch.uint8, device=dev)
+    c = torch.empty(max(cap, 1), dtype=torch.complex128, device=dev)
+    return x, z, k, c
+
+
+def outer_multiply(a: PauliSumSoA, b: PauliSumSoA, *, eps: float = 0.0, combine: bool = True):
+    """A*B on the GPU: raw j-major product (sums.py:144-174) or combined
+    (sums.py:94-120).  Returns a PauliSumSoA on A's device (host in -> host out)."""
+    if eps < 0:
+        raise ValueError("eps must be >= 0")
+    dev, back = _compute_device(a, b)
+    A = a.to(dev).planes()
+    B = b.to(dev).planes()
+    W, ma, mb = A.W, A.M, B.M
+    n_items = ma * mb
+    st = stream_ptr(dev)
+    with torch.cuda.device(dev):
+        if n_items == 0:
+            out = PauliSumSoA.empty(a.n, device=dev)
+        elif not combine:
+            x, z, k, c = _alloc_planes(W, n_items, dev)
+            _native.call("pl_outer_multiply_raw", W, ma, mb,
+                         ptr(A.x), ptr(A.z), ptr(A.k), ptr(A.c), A.ld,
+                         ptr(B.x), ptr(B.z), ptr(B.k), ptr(B.c), B.ld,
+                         ptr(x), ptr(z), ptr(k), ptr(c), x.stride(0), st)
+            out = _new_sum(a.n, x, z, k, c)
+        else:
+            plan = _native.MergePlan()
+            _native.call("pl_outer_plan", W, ma, mb, ptr(A.x), ptr(A.z), A.ld, ptr(B.x),
+                         ptr(B.z), B.ld, C.byref(plan), st)
+            ws = torch.empty(max(int(plan.workspace_bytes), 1), dtype=torch.uint8, device=dev)
+            x, z, k, c = _alloc_planes(W, n_items, dev)
+            cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+            _native.call("pl_outer_multiply_combine", C.byref(plan),
+                         ptr(A.x), ptr(A.z), ptr(A.k), ptr(A.c), A.ld,
+                         ptr(B.x), ptr(B.z), ptr(B.k), ptr(B.c), B.ld,
+                         float(eps), ptr(ws), ws.numel(),
+                         ptr(x), ptr(z), ptr(k), ptr(c), x.stride(0), ptr(cnt), st)
+            m = int(cnt.item())
+            out = _new_sum(a.n, x[:, :m], z[:, :m], k[:m], c[:m])
+    return out.cpu() if back else out
+
+
+def sort_combine(s: PauliSumSoA, *, eps: float = 0.0) -> PauliSumSoA:
+    """sort_and_combine on the GPU (sums.py:94-120, :286-291)."""
+    if eps < 0:
+        raise ValueError("eps must be >= 0")
+    dev, back = _compute_device(s)
+    S = s.to(dev).planes()
+    W, m = S.W, S.M
+    st = stream_ptr(dev)
+    with torch.cuda.device(dev):
+        if m == 0:
+            out = PauliSumSoA.empty(s.n, device=dev)
+        else:
+            plan = _native.MergePlan()
+            _native.call("pl_sort_plan", W, m, ptr(S.x), ptr(S.z), S.ld, C.byref(plan), st)
+            ws = torch.empty(max(int(plan.workspace_bytes), 1), dtype=torch.uint8, device=dev)
+            x, z, k, c = _alloc_planes(W, m, dev)
+            cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+            _native.call("pl_sort_combine", C.byref(plan), ptr(S.x), ptr(S.z), ptr(S.k),
+                         ptr(S.c), S.ld, float(eps), ptr(ws), ws.numel(),
+                         ptr(x), ptr(z), ptr(k), ptr(c), x.stride(0), ptr(cnt), st)
+            mm = int(cnt.item())
+            out = _new_sum(s.n, x[:, :mm], z[:, :mm], k[:mm], c[:mm])
+    return out.cpu() if back else out
+
+
+# ------------------------------------------------------- module functions
+def sum_from_terms(entries: Iterable[TermEntry], n: int | None = None) -> PauliSum:
+    return PauliSum.from_terms(entries, n)
+
+
+def sort_and_combine(s, eps: float = 0.0):
+    """sums.py:484-485."""
+    return s.sort_and_combine(eps)
+
+
+def sum_multiply(a, b, *, threads: int = 1, eps: float = 0.0, combine: bool = True):
+    """sums.py:488-489."""
+    return a.multiply(b, threads=threads, eps=eps, combine=combine)
+
+
+def to_soa(s: PauliSum, device=None) -> PauliSumSoA:
+    return s.to_soa(device)
+
+
+def to_aos(s: PauliSumSoA) -> PauliSum:
+    return s.to_aos()
+
+
+def truncate(s, eps: float):
+    return s.truncate(eps)
