@@ -129,12 +129,13 @@ static int launch_batch_sip(int64_t P, const u64* ax, const u64* az, int64_t lda
 }
 
 // ------------------------------------------------------- raw outer product
-// Complex product without FMA contraction so the result is the plain IEEE
-// (ar*br - ai*bi, ar*bi + ai*br) the reference's numpy multiply computes
-// (sums.py:141).
-__device__ __forceinline__ double2 cmul_rn(double2 a, double2 b) {
-  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
-                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+// Complex product rounded exactly like numpy's complex128 multiply on
+// FMA-capable x86 hosts (the reference's sums.py:141):
+//   re = fma(ar, br, -(ai*bi)),  im = fma(ar, bi, ai*br)
+// (verified bit-for-bit against numpy 2.3.5).
+__device__ __forceinline__ double2 cmul_np(double2 a, double2 b) {
+  return make_double2(__fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y)),
+                      __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x)));
 }
 
 template <int W>
@@ -166,7 +167,7 @@ k_outer_raw(int64_t Ma, int64_t Mb, const u64* __restrict__ ax, const u64* __res
       oz[w * ldo + r] = a_z[w] ^ b_z;
     }
     ok[r] = (uint8_t)(k & 3);
-    oc[r] = cmul_rn(ca, bc[j]);
+    oc[r] = cmul_np(ca, bc[j]);
   }
 }
 

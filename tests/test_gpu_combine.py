@@ -1,0 +1,213 @@
+"""GPU parity: outer product + merge (K2-K4) and sort_and_combine vs reference/oracle.
+
+Contract (north star): merged X/Z bits, phases (all 0) and key sets bit-exact;
+coefficients within 1e-12 relative to the summed magnitudes.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+from oracle import numpy_ref as R
+import paper_2605_25974_b200 as pl
+from paper_2605_25974_b200 import rng
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def check_combined(out, exp):
+    x, z, k, c = out.columns() if hasattr(out, "columns") else out
+    ex, ez, ek, ec = exp
+    assert x.shape == ex.shape, (x.shape, ex.shape)
+    assert np.array_equal(x, ex) and np.array_equal(z, ez)
+    assert not np.asarray(k).any() and not np.asarray(ek).any()
+    scale = max(float(np.abs(ec).sum()), 1e-300)
+    err = float(np.abs(np.asarray(c) - ec).max(initial=0.0))
+    assert err <= TOL * scale, (err, scale)
+
+
+def soa(n, cols, dev):
+    return pl.PauliSumSoA.from_columns(n, *cols, device=dev)
+
+
+def test_outer_c2_golden(cuda):
+    g = golden("outer_c2")
+    a = soa(500, (g["ax"], g["az"], g["af"], g["ac"]), cuda)
+    b = soa(500, (g["bx"], g["bz"], g["bf"], g["bc"]), cuda)
+    check_combined(pl.sum_multiply(a, b), (g["ox"], g["oz"], g["ok"], g["oc"]))
+
+
+def test_outer_hh_golden(cuda):
+    g = golden("outer_hh")
+    h = soa(64, (g["hx"], g["hz"], g["hf"], g["hc"]), cuda)
+    check_combined(h * h, (g["ox"], g["oz"], g["ok"], g["oc"]))
+
+
+def test_simplify_golden(cuda):
+    g = golden("simplify_c5")
+    s = soa(500, (g["x"], g["z"], g["f"], g["c"]), cuda)
+    check_combined(pl.sort_and_combine(s), (g["ox"], g["oz"], g["ok"], g["oc"]))
+
+
+def test_config2_full(cuda):
+    """Config 2 at full size (10^6 pair products) vs the oracle."""
+    a, b = rng.config_columns(2)
+    out = pl.sum_multiply(soa(500, a, cuda), soa(500, b, cuda))
+    check_combined(out, R.outer_combine(*a, *b))
+
+
+def test_config4_scaled(cuda):
+    """Config 4 shape at 1500 x 1500 (2.25e6 products, 96-bit keys, level-2 split)."""
+    a, b = rng.config_columns(4, scale=0.15)
+    out = pl.sum_multiply(soa(500, a, cuda), soa(500, b, cuda))
+    check_combined(out, R.outer_combine(*a, *b))
+
+
+def test_config5_simplify_scaled(cuda):
+    """Config 5 shape (full-width 1000-bit keys, 10% duplicates) at 200k terms."""
+    x, z, f, c = rng.c5_columns(200_000, seed=4)
+    f = np.random.default_rng(3).integers(0, 4, x.shape[0]).astype(np.uint8)
+    out = pl.sort_and_combine(soa(500, (x, z, f, c), cuda))
+    check_combined(out, R.combine(x, z, f, c))
+
+
+def test_dense_random_keys(cuda):
+    """Uniform random 500-qubit strings: every key bit used (KW=16)."""
+    a = rng.random_columns(500, 300, 1)
+    b = rng.random_columns(500, 200, 2)
+    out = pl.sum_multiply(soa(500, a, cuda), soa(500, b, cuda))
+    check_combined(out, R.outer_combine(*a, *b))
+
+
+@pytest.mark.parametrize("n", [1, 64, 100, 256, 1000])
+def test_tiers_hh(cuda, n):
+    h = rng.local_columns(n, 700, rng.SplitMix64(n), min(n, 12), (1, min(n, 4)))
+    s = soa(n, h, cuda)
+    check_combined(s * s, R.outer_combine(*h, *h))
+    check_combined(s.sort_and_combine(), R.combine(*h))
+
+
+def test_runs_longer_than_leaf(cuda):
+    """9000 copies of X (random coefficients and phases) times {X, Y, Z}: three
+    keys each repeated 9000 times (> the 8192-item shared-memory leaf), which
+    no splitter can divide, exercising the in-place global-memory leaf path."""
+    r = np.random.default_rng(9)
+    m = 9000
+    a = (np.ones((m, 1), np.uint64), np.zeros((m, 1), np.uint64),
+         r.integers(0, 4, m).astype(np.uint8), r.normal(size=m) + 1j * r.normal(size=m))
+    b = (np.array([[1], [1], [0]], np.uint64), np.array([[0], [1], [1]], np.uint64),
+         np.array([0, 1, 2], np.uint8), np.array([1.0, -0.5j, 2.0], np.complex128))
+    out = pl.sum_multiply(soa(3, a, cuda), soa(3, b, cuda))
+    check_combined(out, R.outer_combine(*a, *b))
+    # the same with the long runs mixed into many distinct keys
+    h = rng.local_columns(64, 3000, rng.SplitMix64(77), 40, (1, 3))
+    a2 = tuple(np.concatenate([u, v]) for u, v in zip(h, (np.ones((m, 1), np.uint64),
+                                                         np.zeros((m, 1), np.uint64), a[2], a[3])))
+    out2 = pl.sum_multiply(soa(64, a2, cuda), soa(64, b, cuda))
+    check_combined(out2, R.outer_combine(*a2, *b))
+
+
+def test_eps_and_cancellation(cuda):
+    x, z, f, c = rng.c5_columns(5000, seed=1)
+    base = pl.sort_and_combine(soa(500, (x, z, f, c), cuda))
+    ux, uz, uf, uc = base.columns()
+    # a sum with unique keys plus its negation -> empty (SPEC.md:463 (i))
+    s = soa(500, (np.concatenate([ux, ux]), np.concatenate([uz, uz]), np.concatenate([uf, uf]),
+                  np.concatenate([uc, -uc])), cuda)
+    assert len(pl.sort_and_combine(s)) == 0
+    # with repeated keys the reference's own summation order decides which
+    # runs cancel exactly; the GPU reproduces it (numpy reduceat tree)
+    cols = (np.concatenate([x, x]), np.concatenate([z, z]), np.concatenate([f, f]),
+            np.concatenate([c, -c]))
+    check_combined(pl.sort_and_combine(soa(500, cols, cuda)), R.combine(*cols))
+    # shuffled 3x duplication triples the coefficient (ii)
+    perm = np.random.default_rng(0).permutation(3 * len(ux))
+    s3 = soa(500, tuple(np.concatenate([a] * 3)[perm] for a in (ux, uz, uf, uc)), cuda)
+    out3 = pl.sort_and_combine(s3)
+    np.testing.assert_allclose(out3.columns()[3], 3 * uc, rtol=1e-14)
+    # idempotence bit-exact (iii)
+    assert pl.sort_and_combine(base) == base
+    # eps drops small terms
+    out_e = pl.sort_and_combine(soa(500, (x, z, f, c), cuda), eps=0.5)
+    check_combined(out_e, R.combine(x, z, f, c, eps=0.5))
+    with pytest.raises(ValueError):
+        pl.sort_and_combine(soa(500, (x, z, f, c), cuda), eps=-1.0)
+
+
+def test_golden_coefficients_bit_exact(cuda):
+    """Products use numpy's FMA rounding and runs use numpy's reduceat tree, so
+    the merged coefficients equal the reference's bit for bit."""
+    g = golden("outer_hh")
+    h = soa(64, (g["hx"], g["hz"], g["hf"], g["hc"]), cuda)
+    assert np.array_equal((h * h).columns()[3], g["oc"])
+    g = golden("simplify_c5")
+    s = soa(500, (g["x"], g["z"], g["f"], g["c"]), cuda)
+    assert np.array_equal(pl.sort_and_combine(s).columns()[3], g["oc"])
+    g = golden("outer_c2")
+    a = soa(500, (g["ax"], g["az"], g["af"], g["ac"]), cuda)
+    b = soa(500, (g["bx"], g["bz"], g["bf"], g["bc"]), cuda)
+    assert np.array_equal((a * b).columns()[3], g["oc"])
+    g = golden("outer_raw_n500")
+    a = soa(500, (g["ax"], g["az"], g["af"], g["ac"]), cuda)
+    b = soa(500, (g["bx"], g["bz"], g["bf"], g["bc"]), cuda)
+    assert np.array_equal(pl.sum_multiply(a, b, combine=False).columns()[3], g["oc"])
+
+
+def test_empty_and_single(cuda):
+    e = pl.PauliSumSoA.empty(500, device=cuda)
+    one = pl.PauliSumSoA.from_terms([(2.0, "XYZ" + "I" * 497)], device=cuda)
+    assert len(e * one) == 0 and len(one * e) == 0 and len(e.sort_and_combine()) == 0
+    sq = one * one
+    x, z, k, c = sq.columns()
+    assert len(sq) == 1 and not x.any() and not z.any() and c[0] == 4.0
+
+
+def test_determinism_and_host_path(cuda):
+    a, b = rng.config_columns(2, scale=0.5)
+    A, B = soa(500, a, cuda), soa(500, b, cuda)
+    r1 = pl.sum_multiply(A, B)
+    r2 = pl.sum_multiply(A, B, threads=8)
+    assert r1 == r2
+    # host sums in -> host sum out, identical result (end-to-end path)
+    h = pl.sum_multiply(A.cpu(), B.cpu())
+    assert h.device.type == "cpu" and h == r1.cpu()
+    # AoS drop-in
+    aos = pl.PauliSum.from_columns(500, *a).multiply(pl.PauliSum.from_columns(500, *b))
+    assert isinstance(aos, pl.PauliSum) and len(aos) == len(r1)
+
+
+def test_raw_count_exact(cuda):
+    """|output before combine| = |a|*|b| exactly."""
+    a, b = rng.config_columns(2, scale=0.05)
+    raw = pl.sum_multiply(soa(500, a, cuda), soa(500, b, cuda), combine=False)
+    assert len(raw) == 50 * 50
+
+
+def test_dense_matrix_small(cuda):
+    """Outer product equals the dense matrix product at n <= 4."""
+    mats = [np.eye(2), np.array([[0, 1], [1, 0]]), np.array([[1, 0], [0, -1]]),
+            np.array([[0, -1j], [1j, 0]])]
+
+    def dense(s):
+        x, z, k, c = s.columns()
+        tot = 0
+        for t in range(len(s)):
+            m = np.array([[1.0 + 0j]])
+            for q in range(s.n):
+                code = int((x[t, 0] >> np.uint64(q)) & np.uint64(1)) + 2 * int(
+                    (z[t, 0] >> np.uint64(q)) & np.uint64(1))
+                m = np.kron(m, mats[code])
+            tot = tot + c[t] * (1j ** int(k[t])) * m
+        return tot
+
+    r = np.random.default_rng(5)
+    for n in (1, 2, 3, 4):
+        for _ in range(3):
+            la = ["".join(r.choice(list("IXYZ"), n)) for _ in range(int(r.integers(1, 10)))]
+            lb = ["".join(r.choice(list("IXYZ"), n)) for _ in range(int(r.integers(1, 10)))]
+            A = pl.PauliSumSoA.from_terms([(complex(*r.normal(size=2)), l) for l in la], device=cuda)
+            B = pl.PauliSumSoA.from_terms([(complex(*r.normal(size=2)), l) for l in lb], device=cuda)
+            assert np.allclose(dense(A) @ dense(B), dense(A * B), atol=1e-12)
