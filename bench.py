@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Benchmark: outer product + merge (pair-products/s) and commutation checks/s
+at 500 qubits, on B200 (contract: see DESIGN.md "Measurement").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Headline ``value``: BASELINE config 4 (two 10^4-term sums at n=500, weight 8
+on qubits 0..47, seed 3 -> 10^8 pair products), multiply + merge through the
+public API with device-resident inputs, whole-job pair-products/s over N GPUs
+(strong scaling: the 10^8 products are split across ranks by B-term blocks,
+key-range all-to-all over NCCL, local merge).  ``e2e`` is the same call with
+host (pinned) input sums and the merged sum returned to host memory.
+Secondary lines (N=1): config 2, config 1 batched multiply, config 5
+bitmatrix / simplify / grouping.  The CPU baseline is the numpy restatement of
+the reference (oracle/, "port") on a bounded sample, timed on this host.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "pair-products/s (outer product+merge) & commutation checks/s at 500 qubits"
+UNIT = "pair-products/s"
+WORKLOAD = ("C4: outer product + merge of two 10^4-term sums, n=500, weight 8 on qubits "
+            "0..47, complex N(0,1) coefficients, seed 3 (10^8 pair products)")
+L2_FLUSH_BYTES = 512 << 20
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel: str):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu --set full summary."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        v = d.get(kernel)
+        if isinstance(v, dict):
+            return v.get("dram_bytes_per_launch")
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------- CPU side
+def cpu_outer_sample(a, b, m: int, threads: int, repeats: int = 2):
+    """Time the oracle restatement of sum_multiply (sums.py:293-305) on the
+    first m x m terms; returns (pair-products/s, seconds per run)."""
+    from oracle import numpy_ref as R
+
+    A = tuple(x[:m] for x in a)
+    B = tuple(x[:m] for x in b)
+    R.outer_combine(*A, *B, threads=threads)  # warm-up
+    best = None
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        R.outer_combine(*A, *B, threads=threads)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return m * m / best, best
+
+
+def run_reference(args, rank: int, world: int):
+    """--impl reference: the reference's CPU algorithm (numpy port in oracle/;
+    the reference is pure Python and cannot be compiled) on this host's cores."""
+    if rank != 0:
+        return
+    from paper_2605_25974_b200 import rng
+
+    a, b = rng.config_columns(4)
+    threads = os.cpu_count() or 1
+    m = args.cpu_sample
+    times = []
+    from oracle import numpy_ref as R
+
+    A = tuple(x[:m] for x in a)
+    B = tuple(x[:m] for x in b)
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        R.outer_combine(*A, *B, threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = m * m * len(times) / tot
+    sample = (f"first {m} x {m} terms of the C4 inputs ({m * m} pair products) per step; "
+              f"multiply threaded over {threads} threads like sums.py:158-173, combine single-threaded")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64+c128",
+        "data": "synthetic (seeded SplitMix64 generator, DESIGN.md Inputs)",
+        "config": {"workload": WORKLOAD, "sampled": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- GPU side
+def sum_bytes(s) -> int:
+    m = len(s)
+    return 2 * s.words * 8 * m + m + 16 * m
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1000)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_25974_b200 as pl
+    from paper_2605_25974_b200 import _native, rng
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+
+    def barrier():
+        if group is not None:
+            dist.barrier(device_ids=[local])
+
+    # ---- inputs (identical on every rank)
+    a_cols, b_cols = rng.config_columns(4)
+    A = pl.PauliSumSoA.from_columns(500, *a_cols, device=dev)
+    B = pl.PauliSumSoA.from_columns(500, *b_cols, device=dev)
+    n_items = len(A) * len(B)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    if world > 1:
+        from paper_2605_25974_b200 import dist as pdist
+
+        def step():
+            return pdist.sharded_outer_multiply(A, B, group=group)
+    else:
+        def step():
+            return pl.outer_multiply(A, B)
+
+    for _ in range(args.warmup):
+        out = step()
+    torch.cuda.synchronize()
+    del out
+
+    # ---- timed region: K steps, each bracketed by CUDA events on the stream
+    stream = torch.cuda.current_stream(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    counts = []
+    _native.stage_timing(True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)                    # evict L2 between steps
+            evs[i][0].record(stream)
+            out = step()
+            evs[i][1].record(stream)
+            counts.append(len(out))
+            del out
+        torch.cuda.synchronize()
+    barrier()
+    _native.stage_timing(False)
+    stages = _native.stage_times()
+    step_ms = [s.elapsed_time(e) for s, e in evs]
+    tot_ms = sum(step_ms)
+    if group is not None:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = n_items * args.steps / (tot_ms / 1e3)
+
+    # dominant kernel roofline (k_leaves: read items, write merged records)
+    plan = pl.sums.LAST_PLAN or {}
+    kw = plan.get("key_words", 2)
+    leaf_ms = [ms for nm, ms in stages if nm == "k_leaves"]
+    hbm, peak_kind = measured_peaks()
+    roofline = None
+    if leaf_ms:
+        local_items = plan.get("n_items", n_items)
+        local_out = counts[-1]
+        algo = local_items * (8 * kw + 4) + local_out * (16 * 8 + 1 + 16)
+        avg = statistics.mean(leaf_ms) / 1e3
+        achieved = algo / avg / 1e9
+        roofline = {"kernel": "k_leaves", "bound": "hbm", "achieved": achieved, "peak": hbm,
+                    "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic("k_leaves"),
+                    "peak_source": peak_kind,
+                    "algorithmic_bytes_per_launch": algo,
+                    "bytes_per_unit": f"{8 * kw + 4} B item read + {16 * 8 + 17} B per merged term",
+                    "avg_launch_ms": avg * 1e3}
+    stage_share = {}
+    for nm, ms in stages:
+        stage_share[nm] = stage_share.get(nm, 0.0) + ms
+    stage_share = {k: round(v / max(tot_ms, 1e-9), 4) for k, v in stage_share.items()}
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        Ah = A.cpu()
+        Bh = B.cpu()
+        Ah = pl.PauliSumSoA(500, Ah.x.pin_memory(), Ah.z.pin_memory(), Ah.flags.pin_memory(),
+                            Ah.coeffs.pin_memory(), validate=False)
+        Bh = pl.PauliSumSoA(500, Bh.x.pin_memory(), Bh.z.pin_memory(), Bh.flags.pin_memory(),
+                            Bh.coeffs.pin_memory(), validate=False)
+
+        def e2e_step():
+            if world > 1:
+                return pdist.sharded_outer_multiply(Ah, Bh, group=group, device=dev)
+            return pl.sum_multiply(Ah, Bh)
+
+        r = e2e_step()                                   # warm-up (pinned pools)
+        d2h = sum_bytes(r)
+        del r
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ne = max(1, min(args.steps, 3))
+        for _ in range(ne):
+            r = e2e_step()
+            del r
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        if group is not None:
+            t = torch.tensor([el], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": n_items * ne / el, "unit": UNIT,
+               "h2d_bytes_per_step": sum_bytes(A) + sum_bytes(B), "d2h_bytes_per_step": d2h,
+               "ms_per_step": 1e3 * el / ne}
+
+    # ---- CPU baseline and secondary workloads (rank 0 at N=1 only)
+    cpu = None
+    secondary = {}
+    if world == 1 and rank == 0:
+        if not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            v, sec = cpu_outer_sample(a_cols, b_cols, args.cpu_sample, threads)
+            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                   "sample": (f"first {args.cpu_sample} x {args.cpu_sample} terms of the C4 "
+                              f"inputs ({args.cpu_sample ** 2} pair products), min of 2 runs "
+                              f"({sec:.2f} s each); multiply threaded over {threads} threads, "
+                              f"combine single-threaded (sums.py:158-173, :94-120)")}
+        if not args.no_secondary:
+            from bench_secondary import run_secondary
+
+            secondary = run_secondary(dev, flush)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u64+c128", "data": "synthetic (seeded SplitMix64 generator, DESIGN.md Inputs)",
+            "config": {"workload": WORKLOAD, "pair_products_per_step": n_items,
+                       "merged_terms": counts[-1] if counts else None,
+                       "l2": "512 MiB buffer written between timed steps; working set >> L2",
+                       "key_words": kw, "buckets": plan.get("n_buckets")},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": len(stages), "clocks": clk.summary(), "stage_share": stage_share,
+            "secondary": secondary,
+        }
+        print(json.dumps(line), flush=True)
+    if group is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,153 @@
+"""Secondary bench lines (N=1): the other BASELINE configs on the same B200.
+
+Each entry: {"value", "unit", "ms_per_step", ...} timed with CUDA events on the
+launching stream after warm-up, L2 flushed between timed repetitions.
+"""
+
+from __future__ import annotations
+
+import json
+import statistics
+from pathlib import Path
+
+import numpy as np
+import torch
+
+import paper_2605_25974_b200 as pl
+from paper_2605_25974_b200 import _native, rng
+
+ROOT = Path(__file__).resolve().parent
+
+
+def _hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    return float(json.loads(p.read_text()).get("hbm_gbs", 6650.0)) if p.exists() else 6650.0
+
+
+def _timed(fn, dev, flush, reps: int, warm: int = 2):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream(dev)
+    ms = []
+    for i in range(reps):
+        flush.fill_(i & 0xFF)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        fn()
+        b.record(st)
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+    return ms
+
+
+def c2(dev, flush):
+    a, b = rng.config_columns(2)
+    A = pl.PauliSumSoA.from_columns(500, *a, device=dev)
+    B = pl.PauliSumSoA.from_columns(500, *b, device=dev)
+    ms = _timed(lambda: pl.outer_multiply(A, B), dev, flush, 10)
+    t = statistics.mean(ms)
+    return {"workload": "C2: 1000 x 1000 outer product + merge, 4-local on qubits 0..23, seed 1",
+            "value": 1e6 / (t / 1e3), "unit": "pair-products/s", "ms_per_step": t}
+
+
+def c1(dev, flush):
+    out = {}
+    for P, label in ((65536, "C1: 65,536 pairs, n=500, seed 0/1"),
+                     (1 << 24, "C1 shape at P=2^24 (HBM roofline check)")):
+        a = rng.random_columns(500, min(P, 65536), 0)
+        b = rng.random_columns(500, min(P, 65536), 1)
+        reps_p = P // min(P, 65536)
+        ax = torch.from_numpy(np.ascontiguousarray(np.tile(a[0].T, (1, reps_p))).view(np.int64)).to(dev)
+        az = torch.from_numpy(np.ascontiguousarray(np.tile(a[1].T, (1, reps_p))).view(np.int64)).to(dev)
+        bx = torch.from_numpy(np.ascontiguousarray(np.tile(b[0].T, (1, reps_p))).view(np.int64)).to(dev)
+        bz = torch.from_numpy(np.ascontiguousarray(np.tile(b[1].T, (1, reps_p))).view(np.int64)).to(dev)
+        ak = torch.zeros(P, dtype=torch.uint8, device=dev)
+        bk = torch.zeros(P, dtype=torch.uint8, device=dev)
+        inner = 200 if P <= 65536 else 5
+
+        def run():
+            for _ in range(inner):
+                pl.batch_multiply(ax, az, ak, bx, bz, bk)
+
+        ms = _timed(run, dev, flush, 5)
+        t = statistics.mean(ms) / inner
+        pairs = P / (t / 1e3)
+        gbs = 387 * P / (t / 1e3) / 1e9
+        out["c1" if P == 65536 else "c1_2e24"] = {
+            "workload": label, "value": pairs, "unit": "pairs/s", "ms_per_launch": t,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": _hbm(), "unit": "GB/s",
+                         "frac": gbs / _hbm(), "bytes_per_unit": "387 B/pair (W=8)"}}
+    return out
+
+
+def c5(dev, flush):
+    x, z, f, c = rng.c5_columns(1_000_000, seed=4)
+    S = pl.PauliSumSoA.from_columns(500, x, z, f, c, device=dev)
+    M = len(S)
+    res = {}
+    # simplify
+    ms = _timed(lambda: pl.sort_combine(S), dev, flush, 5)
+    t = statistics.mean(ms)
+    res["c5_simplify"] = {"workload": "C5 sort_and_combine, 10^6 terms, seed 4",
+                          "value": M / (t / 1e3), "unit": "terms/s", "ms_per_step": t,
+                          "merged_terms": len(pl.sort_combine(S))}
+    # full commutation bitmatrix, row chunks into one reused output buffer
+    rows = 65536
+    nw = (M + 31) // 32
+    buf = torch.empty((rows, nw), dtype=torch.int32, device=dev)
+
+    def bitmatrix():
+        for r0 in range(0, M, rows):
+            r = min(rows, M - r0)
+            pl.commutation_bitmatrix(S, row0=r0, rows=r, out=buf[:r])
+
+    _native.stage_timing(True)
+    ms = _timed(bitmatrix, dev, flush, 2, warm=1)
+    _native.stage_timing(False)
+    st = _native.stage_times()
+    kms = [m for n, m in st if n.startswith("k_bitmatrix")]
+    t = statistics.mean(ms)
+    checks = float(M) * M
+    out_bytes = M * nw * 4
+    # dominant kernel: bytes = 1 bit per check written (+ its row lists), vs HBM peak
+    kt = sum(kms) / max(len(ms) + 1, 1) if kms else None
+    res["c5_bitmatrix"] = {
+        "workload": "C5 full commutation bitmatrix 10^6 x 10^6 (row chunks of 65536)",
+        "value": checks / (t / 1e3), "unit": "checks/s", "ms_per_step": t,
+        "output_bytes": out_bytes,
+        "roofline": {"bound": "hbm", "achieved": out_bytes / (t / 1e3) / 1e9, "peak": _hbm(),
+                     "unit": "GB/s", "frac": out_bytes / (t / 1e3) / 1e9 / _hbm(),
+                     "bytes_per_unit": "1 bit written per check"},
+    }
+    return res
+
+
+def c3(dev, flush):
+    x, z, f, c = rng.config_columns(3)
+    S = pl.PauliSumSoA.from_columns(100, x, z, f, c, device=dev)
+    try:
+        gof, ng, pc = pl.group_assignment(S)
+    except _native.NativeLibraryError as e:
+        return {"c3_grouping": {"skipped": str(e)[:120]}}
+    ms = _timed(lambda: pl.group_assignment(S), dev, flush, 2, warm=1)
+    t = statistics.mean(ms)
+    checks = int(pc.item())
+    return {"c3_grouping": {"workload": "C3 greedy grouping, JW-style n=100, 10^5 terms, seed 2",
+                            "value": checks / (t / 1e3), "unit": "reference pair_checks/s",
+                            "ms_per_step": t, "groups": int(ng.item()), "pair_checks": checks}}
+
+
+def run_secondary(dev, flush) -> dict:
+    out = {}
+    for fn in (c2, c1, c5, c3):
+        try:
+            r = fn(dev, flush)
+        except Exception as e:  # keep the headline line even if a side metric fails
+            r = {fn.__name__: {"error": f"{type(e).__name__}: {e}"[:200]}}
+        if "workload" in r:
+            out[fn.__name__] = r
+        else:
+            out.update(r)
+        torch.cuda.empty_cache()
+    return out

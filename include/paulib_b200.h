@@ -170,6 +170,16 @@ int pl_group_greedy(int W, int64_t M, const uint64_t* x, const uint64_t* z, int6
                     int32_t* group_of, int32_t* n_groups, int64_t* pair_checks,
                     void* workspace, size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Stage timing (instrumentation for bench.py).  While enabled, multi-kernel
+ * entry points record a CUDA event pair around every kernel they launch, on
+ * the launching stream.  pl_stage_times() waits for the recorded events and
+ * returns up to `max` (name, milliseconds) pairs in launch order (names are
+ * NUL-terminated, 32 bytes each), then clears the record.  Returns the count.
+ */
+int pl_stage_timing(int enable);
+int pl_stage_times(char* names, float* ms, int max);
+
 #ifdef __cplusplus
 }
 #endif

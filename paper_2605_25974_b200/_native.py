@@ -70,7 +70,22 @@ SIGNATURES = {
     "pl_bitmatrix_workspace_bytes": (_L, [_I, _L]),
     "pl_group_workspace_bytes": (_L, [_I, _L]),
     "pl_group_greedy": (_I, [_I, _L, _P, _P, _L, _P, _P, _P, _P, _S, _P]),
+    "pl_stage_timing": (_I, [_I]),
+    "pl_stage_times": (_I, [_P, _P, _I]),
 }
+
+
+def stage_timing(enable: bool) -> None:
+    load().pl_stage_timing(1 if enable else 0)
+
+
+def stage_times(max_stages: int = 4096) -> list[tuple[str, float]]:
+    """(kernel name, ms) for every kernel launched since timing was enabled."""
+    names = C.create_string_buffer(32 * max_stages)
+    ms = (C.c_float * max_stages)()
+    n = load().pl_stage_times(names, ms, max_stages)
+    raw = names.raw
+    return [(raw[32 * i:32 * i + 32].split(b"\0", 1)[0].decode(), float(ms[i])) for i in range(n)]
 
 _lib = None
 _load_error: str | None = None

@@ -239,6 +239,7 @@ static int launch_bitmatrix(int64_t M, const u64* x, const u64* z, int64_t ld, i
       for (int64_t cbase = 0; cbase < colblocks; cbase += 65535) {
         const int64_t nblk = colblocks - cbase < 65535 ? colblocks - cbase : 65535;
         dim3 grid((unsigned)nblk, (unsigned)splits);
+        StageTimer t_(st, "k_bitmatrix_lists");
         kern<<<grid, 1024, smem, st>>>(x, z, ld, M, row0, rows, col0 + cbase * kColsPerCta,
                                        cols - cbase * kColsPerCta, off, list,
                                        bits + cbase * (kColsPerCta / 32), ld_bits, rps);
@@ -254,6 +255,7 @@ static int launch_bitmatrix(int64_t M, const u64* x, const u64* z, int64_t ld, i
   for (int64_t rb = 0; rb < rowblocks; rb += 65535) {
     const int64_t nrb = rowblocks - rb < 65535 ? rowblocks - rb : 65535;
     dim3 grid((unsigned)colblocks, (unsigned)nrb);
+    StageTimer t_(st, "k_bitmatrix_direct");
     k_bitmatrix_direct<W><<<grid, kDirectRows, 0, st>>>(
         x, z, ld, M, row0 + rb * kDirectRows, rows - rb * kDirectRows, col0, cols,
         bits + rb * kDirectRows * ld_bits, ld_bits);

@@ -994,6 +994,7 @@ static int launch_masks(const u64* x, const u64* z, int64_t ld, int64_t m, u64* 
   if (m == 0) return PL_OK;
   int64_t blocks = ceil_div(m, 256);
   if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
+  StageTimer t_(st, "k_or_masks");
   k_or_masks<W><<<(unsigned)blocks, 256, 0, st>>>(x, z, ld, m, out);
   PLB_CHECK_LAUNCH("k_or_masks");
   return PL_OK;
@@ -1083,6 +1084,7 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const O
   if (D.nb1 > 1) {
     const size_t sm1 = (size_t)D.nsamp * (8 * KW + 4) + 16;
     if (set_smem(k_sample<W, KW, MODE>, sm1)) return PL_ERR_CUDA;
+    StageTimer t_(st, "k_sample");
     k_sample<W, KW, MODE><<<1, kLeafThreads, sm1, st>>>(L, D, S, C);
     PLB_CHECK_LAUNCH("k_sample");
   }
@@ -1097,23 +1099,33 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const O
   }
   if (D.nb1 > 1) {
     if (set_smem(k_count<W, KW, MODE>, gsm)) return PL_ERR_CUDA;
+    StageTimer t_(st, "k_count");
     k_count<W, KW, MODE><<<ggrid, kGenThreads, gsm, st>>>(L, D, S, C);
     PLB_CHECK_LAUNCH("k_count");
   }
   // 3. bucket bases / leaves
-  k_buckets<<<1, 1024, 0, st>>>(D, C, O.count);
-  PLB_CHECK_LAUNCH("k_buckets");
+  {
+    StageTimer t_(st, "k_buckets");
+    k_buckets<<<1, 1024, 0, st>>>(D, C, O.count);
+    PLB_CHECK_LAUNCH("k_buckets");
+  }
   // 4. scatter
   if (set_smem(k_scatter<W, KW, MODE>, gsm)) return PL_ERR_CUDA;
-  k_scatter<W, KW, MODE><<<ggrid, kGenThreads, gsm, st>>>(L, D, S, C);
-  PLB_CHECK_LAUNCH("k_scatter");
+  {
+    StageTimer t_(st, "k_scatter");
+    k_scatter<W, KW, MODE><<<ggrid, kGenThreads, gsm, st>>>(L, D, S, C);
+    PLB_CHECK_LAUNCH("k_scatter");
+  }
   // 5. level-2 split of oversized buckets
   const int s2cap = (int)P.reserved[1];
   const size_t ssm = (size_t)s2cap * (8 * KW + 4) + 8 + (size_t)8 * KW * D.max_sub +
                      (size_t)8 * D.max_sub + 64;
   if (set_smem(k_split<KW>, ssm)) return PL_ERR_CUDA;
-  k_split<KW><<<D.nb1, kSplitThreads, ssm, st>>>(D, C, s2cap);
-  PLB_CHECK_LAUNCH("k_split");
+  {
+    StageTimer t_(st, "k_split");
+    k_split<KW><<<D.nb1, kSplitThreads, ssm, st>>>(D, C, s2cap);
+    PLB_CHECK_LAUNCH("k_split");
+  }
   // 6. leaves
   constexpr int CH = (kSortSmemBytes / ((8 * KW + 4) * kLeafThreads)) >= 16 ? 16
                      : (kSortSmemBytes / ((8 * KW + 4) * kLeafThreads)) >= 8 ? 8
@@ -1123,6 +1135,7 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const O
   auto lk = k_leaves<W, KW, MODE, CH>;
   if (set_smem(lk, lsm)) return PL_ERR_CUDA;
   int grid = num_sms();
+  StageTimer t_(st, "k_leaves");
   lk<<<grid, kLeafThreads, lsm, st>>>(L, D, S, C, O);
   PLB_CHECK_LAUNCH("k_leaves");
   return PL_OK;

@@ -37,6 +37,29 @@ int cuda_status(cudaError_t e, const char* what);
     if (_e != cudaSuccess) return ::plb::cuda_status(_e, #call); \
   } while (0)
 
+// ------------------------------------------------------------ stage timing
+// RAII event pair around one kernel launch when pl_stage_timing(1) is on.
+bool stage_timing_enabled();
+void stage_record(const char* name, cudaEvent_t a, cudaEvent_t b);
+struct StageTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t st;
+  const char* name;
+  StageTimer(cudaStream_t s, const char* n) : st(s), name(n) {
+    if (stage_timing_enabled()) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~StageTimer() {
+    if (a) {
+      cudaEventRecord(b, st);
+      stage_record(name, a, b);
+    }
+  }
+};
+
 // ----------------------------------------------------------- bit helpers
 __device__ __forceinline__ int popc64(u64 v) { return __popcll(v); }
 

@@ -413,6 +413,29 @@ def _compute_device(*sums: PauliSumSoA) -> tuple[torch.device, bool]:
     return cuda_device(), True
 
 
+LAST_PLAN: dict | None = None  # instrumentation: layout of the most recent merge
+
+
+def _remember(plan) -> None:
+    global LAST_PLAN
+    LAST_PLAN = {k: int(getattr(plan, k)) for k in
+                 ("W", "mode", "n_items", "key_words", "key_bits", "n_buckets", "n_samples",
+                  "leaf_cap", "leaf_target", "max_sub", "workspace_bytes")}
+
+
+def _download(s: PauliSumSoA) -> PauliSumSoA:
+    """Device result -> host sum through pinned staging buffers (torch's caching
+    host allocator recycles them), one async copy per array, then one sync."""
+    def pinned(t):
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        return h
+
+    x, z, k, c = (pinned(t) for t in (s.x, s.z, s.flags, s.coeffs))
+    torch.cuda.current_stream(s.device).synchronize()
+    return _new_sum(s.n, x, z, k, c)
+
+
 def _new_sum(n, x, z, k, c) -> PauliSumSoA:
     out = object.__new__(PauliSumSoA)
     out.n, out.tier = int(n), tier_for(n)
@@ -453,6 +476,7 @@ def outer_multiply(a: PauliSumSoA, b: PauliSumSoA, *, eps: float = 0.0, combine:
             plan = _native.MergePlan()
             _native.call("pl_outer_plan", W, ma, mb, ptr(A.x), ptr(A.z), A.ld, ptr(B.x),
                          ptr(B.z), B.ld, C.byref(plan), st)
+            _remember(plan)
             ws = torch.empty(max(int(plan.workspace_bytes), 1), dtype=torch.uint8, device=dev)
             x, z, k, c = _alloc_planes(W, n_items, dev)
             cnt = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -463,7 +487,7 @@ def outer_multiply(a: PauliSumSoA, b: PauliSumSoA, *, eps: float = 0.0, combine:
                          ptr(x), ptr(z), ptr(k), ptr(c), x.stride(0), ptr(cnt), st)
             m = int(cnt.item())
             out = _new_sum(a.n, x[:, :m], z[:, :m], k[:m], c[:m])
-    return out.cpu() if back else out
+    return _download(out) if back else out
 
 
 def sort_combine(s: PauliSumSoA, *, eps: float = 0.0) -> PauliSumSoA:
@@ -480,6 +504,7 @@ def sort_combine(s: PauliSumSoA, *, eps: float = 0.0) -> PauliSumSoA:
         else:
             plan = _native.MergePlan()
             _native.call("pl_sort_plan", W, m, ptr(S.x), ptr(S.z), S.ld, C.byref(plan), st)
+            _remember(plan)
             ws = torch.empty(max(int(plan.workspace_bytes), 1), dtype=torch.uint8, device=dev)
             x, z, k, c = _alloc_planes(W, m, dev)
             cnt = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -488,7 +513,7 @@ def sort_combine(s: PauliSumSoA, *, eps: float = 0.0) -> PauliSumSoA:
                          ptr(x), ptr(z), ptr(k), ptr(c), x.stride(0), ptr(cnt), st)
             mm = int(cnt.item())
             out = _new_sum(s.n, x[:, :mm], z[:, :mm], k[:mm], c[:mm])
-    return out.cpu() if back else out
+    return _download(out) if back else out
 
 
 # ------------------------------------------------------- module functions
