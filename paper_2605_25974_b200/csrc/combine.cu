@@ -709,166 +709,50 @@ __device__ __forceinline__ bool keep_sum(double2 s, double eps) {
   return hypot(s.x, s.y) > eps;
 }
 
-// thread 0: publish this leaf's kept count, return the exclusive prefix
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Decoupled look-back over leaves, run by one full warp: publish this leaf's
+// kept count, then scan predecessors 32 at a time (flag 1 = aggregate only,
+// 2 = inclusive prefix, 0 = not yet published) until an inclusive prefix is
+// found.  Returns the exclusive prefix (valid in every lane).
 __device__ uint64_t leaf_lookback(unsigned long long* status, uint32_t leaf, uint64_t agg) {
   constexpr unsigned long long kAgg = 1ull << 62, kPre = 2ull << 62, kVal = (1ull << 62) - 1;
+  const int lane = threadIdx.x & 31;
   if (leaf == 0) {
-    atomicExch(&status[0], kPre | agg);
+    if (lane == 0) st_relaxed_gpu(&status[0], kPre | agg);
     return 0;
   }
-  atomicExch(&status[leaf], kAgg | agg);
+  if (lane == 0) st_relaxed_gpu(&status[leaf], kAgg | agg);
   uint64_t excl = 0;
-  int64_t q = (int64_t)leaf - 1;
+  int64_t base = (int64_t)leaf - 1;
   for (;;) {
-    const unsigned long long v = *(volatile unsigned long long*)&status[q];
-    const unsigned long long f = v >> 62;
-    if (f == 0) continue;
-    excl += v & kVal;
-    if (f == 2) break;
-    --q;
+    const int64_t idx = base - lane;
+    const unsigned long long v = idx >= 0 ? ld_relaxed_gpu(&status[idx]) : kPre;
+    const unsigned f = (unsigned)(v >> 62);
+    const unsigned inc = __ballot_sync(0xffffffffu, f == 2);
+    const unsigned zero = __ballot_sync(0xffffffffu, f == 0);
+    const int first = inc ? __ffs(inc) - 1 : 32;  // nearest inclusive predecessor
+    const unsigned need = first == 32 ? 0xffffffffu : ((2u << first) - 1u);
+    if (zero & need) continue;  // a needed predecessor has not published yet
+    unsigned long long c = (lane <= first) ? (v & kVal) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    excl += c;
+    if (first < 32) break;
+    base -= 32;
   }
-  atomicExch(&status[leaf], kPre | (excl + agg));
+  if (lane == 0) st_relaxed_gpu(&status[leaf], kPre | (excl + agg));
   return excl;
 }
 
-template <int W, int KW, int MODE, int CH>
-__global__ void __launch_bounds__(kLeafThreads, 1)
-k_leaves(Layout L, Dims D, SrcA S, Ctl C, OutP O) {
-  extern __shared__ u64 sm[];
-  constexpr int cap = CH * kLeafThreads;
-  u64* SK = sm;
-  uint32_t* SI = reinterpret_cast<uint32_t*>(SK + (int64_t)KW * cap);
-  __shared__ uint32_t s_leaf;
-  __shared__ uint32_t s_warp[kLeafThreads / 32];
-  __shared__ uint64_t s_base;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const uint32_t n_leaves = *C.n_leaves;
-
-  for (;;) {
-    if (tid == 0) s_leaf = atomicAdd(C.leaf_ctr, 1u);
-    __syncthreads();
-    const uint32_t leaf = s_leaf;
-    if (leaf >= n_leaves) break;
-    const uint4 dsc = C.leaf_desc[leaf];
-    const int n = (int)dsc.z;
-    const u64* GK = (dsc.x == 1 ? C.k1 : C.k2) + dsc.y;
-    const uint32_t* GI = (dsc.x == 1 ? C.i1 : C.i2) + dsc.y;
-    const bool local = n <= cap;
-    u64* K;
-    uint32_t* I;
-    int64_t stride;
-    if (local) {
-      for (int t = tid; t < n; t += blockDim.x) {
-#pragma unroll
-        for (int d = 0; d < KW; ++d) SK[d * cap + t] = GK[d * D.n + t];
-        SI[t] = GI[t];
-      }
-      K = SK;
-      I = SI;
-      stride = cap;
-    } else {  // oversized leaf: sort in place in global memory
-      K = const_cast<u64*>(GK);
-      I = const_cast<uint32_t*>(GI);
-      stride = D.n;
-    }
-    __syncthreads();
-    if (n > 1) bitonic_sort<KW>(K, I, stride, n);
-
-    // ---- pass 1: run sums (kept in registers when the leaf is one tile)
-    constexpr int tile = CH * kLeafThreads;
-    double2 sums[CH];
-    uint32_t keep_bits = 0;
-    uint32_t my_cnt = 0;
-    for (int t0 = 0; t0 < n; t0 += tile) {
-      uint32_t kb = 0;
-#pragma unroll
-      for (int j = 0; j < CH; ++j) {
-        const int p = t0 + tid * CH + j;
-        sums[j] = make_double2(0.0, 0.0);
-        if (p < n && (p == 0 || !key_eq<KW>(K, stride, p, p - 1))) {
-          int q = p + 1;
-          while (q < n && key_eq<KW>(K, stride, q, q - 1)) ++q;
-          const double2 s = RunSum<W, KW, MODE>::run(S, D.ma, I, p, q - p);
-          sums[j] = s;
-          if (keep_sum(s, O.eps)) kb |= 1u << j;
-        }
-      }
-      my_cnt += __popc(kb);
-      keep_bits = kb;
-    }
-    // ---- leaf total + look-back
-    uint32_t v = my_cnt;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) s_warp[wid] = v;
-    __syncthreads();
-    if (tid == 0) {
-      uint64_t agg = 0;
-      for (int w = 0; w < kLeafThreads / 32; ++w) agg += s_warp[w];
-      const uint64_t excl = leaf_lookback(C.leaf_status, leaf, agg);
-      s_base = excl;
-      if (leaf == n_leaves - 1) *O.count = (int64_t)(excl + agg);
-    }
-    __syncthreads();
-    // ---- pass 2: write merged terms (single tile: sums from registers)
-    uint64_t out_base = s_base;
-    for (int t0 = 0; t0 < n; t0 += tile) {
-      uint32_t kb = keep_bits;
-      if (n > tile) {  // multi-tile: recompute this tile's sums
-        kb = 0;
-#pragma unroll
-        for (int j = 0; j < CH; ++j) {
-          const int p = t0 + tid * CH + j;
-          if (p < n && (p == 0 || !key_eq<KW>(K, stride, p, p - 1))) {
-            int q = p + 1;
-            while (q < n && key_eq<KW>(K, stride, q, q - 1)) ++q;
-            const double2 s = RunSum<W, KW, MODE>::run(S, D.ma, I, p, q - p);
-            sums[j] = s;
-            if (keep_sum(s, O.eps)) kb |= 1u << j;
-          }
-        }
-      }
-      // block exclusive scan of popc(kb)
-      const uint32_t c = __popc(kb);
-      uint32_t inc = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t tt = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += tt;
-      }
-      __syncthreads();
-      if (lane == 31) s_warp[wid] = inc;
-      __syncthreads();
-      uint32_t wbase = 0, total = 0;
-      for (int w = 0; w < kLeafThreads / 32; ++w) {
-        const uint32_t sw = s_warp[w];
-        if (w < wid) wbase += sw;
-        total += sw;
-      }
-      uint64_t pos = out_base + wbase + inc - c;
-#pragma unroll
-      for (int j = 0; j < CH; ++j) {
-        if (kb >> j & 1) {
-          const int p = t0 + tid * CH + j;
-          u64 key[KW];
-          load_key<KW>(K, stride, p, key);
-#pragma unroll
-          for (int s = 0; s < 2 * W; ++s) {
-            const int len = L.len[s];
-            const u64 w = len ? (get_seg<KW>(key, L.pos[s], len) << L.lo[s]) : 0ull;
-            if (s < W) O.oz[s * O.ldo + pos] = w;
-            else O.ox[(s - W) * O.ldo + pos] = w;
-          }
-          O.ok[pos] = 0;
-          O.oc[pos] = sums[j];
-          ++pos;
-        }
-      }
-      out_base += total;
-    }
-    __syncthreads();
-  }
-}
+#include "merge_leaves.cuh"
 
 // ============================================================== host side
 static inline int64_t align256(int64_t v) { return (v + 255) & ~(int64_t)255; }
@@ -877,18 +761,6 @@ struct WsLayout {
   int64_t split, bcount, bbase, bcursor, leaf_off, n_leaves, leaf_ctr, leaf_desc, leaf_status,
       k1, i1, k2, i2, total;
 };
-
-static int leaf_ch_for(int KW) {
-  // per-thread chunk: cap = CH * kLeafThreads items of (8 KW + 4) bytes in <= kSortSmemBytes
-  int ch = kSortSmemBytes / ((8 * KW + 4) * kLeafThreads);
-  if (ch > 16) ch = 16;
-  if (ch < 1) ch = 1;
-  // round down to a supported instantiation
-  const int allowed[] = {16, 8, 4, 2, 1};
-  for (int a : allowed)
-    if (ch >= a) return a;
-  return 1;
-}
 
 static WsLayout ws_layout(const pl_merge_plan& P) {
   WsLayout w{};
@@ -937,12 +809,11 @@ static void finish_plan(pl_merge_plan* P, const u64* masks /* z[W] then x[W] */)
   P->key_words = key_words_for_bits(pos > 0 ? pos : 1);
   P->reserved[0] = active;
   const int KW = P->key_words;
-  const int ch = leaf_ch_for(KW);
-  const int cap = ch * kLeafThreads;
+  const int cap = leaf_cap_for(KW);
   P->leaf_cap = cap;
-  P->leaf_target = cap / 3 > 1 ? cap / 3 : 1;
-  // one-CTA sample capacity (same shared-memory budget as a leaf)
-  const int scap = cap;
+  P->leaf_target = cap / 3;  // headroom: sampled splitters vary bucket sizes
+  // one-CTA sample capacity: the sampler sorts in up to kSortSmemBytes
+  const int scap = std::min(8192, kSortSmemBytes / (8 * KW + 4));
   const int64_t n = P->n_items;
   int64_t nb1 = 1;
   if (n > cap) {
@@ -954,8 +825,9 @@ static void finish_plan(pl_merge_plan* P, const u64* masks /* z[W] then x[W] */)
   P->n_buckets = (int)nb1;
   P->n_samples = nb1 > 1 ? (int)std::min<int64_t>(n, std::min<int64_t>(scap, nb1 * kSampleOversample)) : 0;
   // level-2 sample capacity bounds the sub-bucket count
-  const int s2cap = std::max(64, std::min(4096, (96 * 1024) / (8 * KW + 4)));
-  P->max_sub = std::max(1, std::min(1024, s2cap / 4));
+  // level-2 sample (one CTA, <= 160 KB): >= 8 samples per sub-bucket
+  const int s2cap = std::max(64, std::min(8192, (160 * 1024) / (8 * KW + 4)));
+  P->max_sub = std::max(1, std::min(1024, s2cap / 8));
   P->reserved[1] = s2cap;
   P->workspace_bytes = ws_layout(*P).total;
 }
@@ -1127,16 +999,12 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const O
     PLB_CHECK_LAUNCH("k_split");
   }
   // 6. leaves
-  constexpr int CH = (kSortSmemBytes / ((8 * KW + 4) * kLeafThreads)) >= 16 ? 16
-                     : (kSortSmemBytes / ((8 * KW + 4) * kLeafThreads)) >= 8 ? 8
-                     : (kSortSmemBytes / ((8 * KW + 4) * kLeafThreads)) >= 4 ? 4
-                     : (kSortSmemBytes / ((8 * KW + 4) * kLeafThreads)) >= 2 ? 2 : 1;
-  const size_t lsm = (size_t)CH * kLeafThreads * (8 * KW + 4) + 16;
-  auto lk = k_leaves<W, KW, MODE, CH>;
+  const size_t lsm = leaf_smem_bytes(KW);
+  auto lk = k_leaves<W, KW, MODE>;
   if (set_smem(lk, lsm)) return PL_ERR_CUDA;
-  int grid = num_sms();
+  const int grid = 4 * num_sms();
   StageTimer t_(st, "k_leaves");
-  lk<<<grid, kLeafThreads, lsm, st>>>(L, D, S, C, O);
+  lk<<<grid, kLeafThreads2, lsm, st>>>(L, D, S, C, O);
   PLB_CHECK_LAUNCH("k_leaves");
   return PL_OK;
 }
