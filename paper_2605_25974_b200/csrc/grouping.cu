@@ -1,9 +1,612 @@
-// K6 greedy grouping — placeholder until the batched kernel lands.
+// K6 — greedy first-fit commutation grouping, exactly the reference's
+// _greedy_over (grouping.py:67-83): term t, in index order, joins the first
+// group (creation order) all of whose members commute with it, else opens a
+// new group; pair_checks counts the members of every group tried (:75-76).
+//
+// Group state is kept TRANSPOSED: for group g, member-chunk c (members
+// 64c..64c+63) stores one uint64 per key bit e in [0, 128W):
+//   T_g[c][e] bit s  =  partner bit of member 64c+s for a term entry e, where
+//   a term's x-bit at qubit q (entry e = q) pairs with the member's z-bit at q
+//   and a term's z-bit at q (entry e = 64W + q) with the member's x-bit at q.
+// "t commutes with every member of g" <=> for every chunk c the XOR over t's
+// set-bit entries of T_g[c][e] is zero (bit s = symplectic parity with member
+// s).  Cost per (term, group) test = |entries of t| loads of chunk 0 (members
+// 0..63); later chunks are only read when chunk 0 already fits.
+//
+// Exactness under parallelism: terms are processed in batches of B = 1024.
+//   fit     : fit0[t][g] for every batch term t and every group g existing at
+//             batch start (parallel over groups x terms);
+//   firstk  : first 4 fitting groups per term (warp per term);
+//   anti    : intra-batch anti-commutation rows (row-list bitmatrix kernel);
+//   resolve : one warp replays the batch in order; a candidate group is
+//             rejected only if an earlier batch member already placed in it
+//             anti-commutes with t (member masks in shared memory), and
+//             groups created inside the batch are tried after all older
+//             ones, in creation order -- exactly the sequential first-fit;
+//   update  : append the batch members to their groups' transposed chunks and
+//             add each term's reference pair_checks contribution
+//             #{u < t : group(u) <= group(t)}.
+#include <algorithm>
+
+#include "bitmatrix_kernels.cuh"
 #include "common.cuh"
+#include "scan.cuh"
+
+namespace plb {
+
+constexpr int kGB = 1024;              // batch size (terms)
+constexpr int kGAW = kGB / 32;         // anti-row words per term
+constexpr int kGK = 4;                 // first-k fitting groups kept per term
+constexpr int kSlotChunks = kGB / 64 + 2;
+constexpr int kHash = 2048;            // resolver hash slots (power of 2)
+
+struct GCtx {
+  int W;
+  int64_t M;
+  int64_t gcap, ccap;                  // group / chunk capacity
+  const u64 *x, *z;
+  int64_t ld;
+  // CSR entries of every term
+  const uint32_t* off;                 // M + 1
+  const uint16_t* list;
+  // groups
+  uint32_t* gsize;                     // gcap
+  int32_t* gfirst;                     // gcap
+  int32_t* glast;                      // gcap
+  uint32_t* gpre;                      // gcap: inclusive prefix of sizes at batch start
+  // chunk pool: ccap chunks of 128W uint64 + next links
+  u64* pool;
+  int32_t* cnext;
+  // scalars
+  uint32_t* gcur;                      // groups so far
+  uint32_t* pool_next;
+  uint32_t* overflow;
+  unsigned long long* checks;
+  // per batch
+  uint32_t* fit0;                      // [kGB][gw_stride]
+  int64_t gw_stride;
+  int32_t* fitk;                       // [kGB][kGK]
+  int32_t* nfit;                       // [kGB]
+  uint32_t* anti;                      // [kGB][kGAW]
+  uint32_t* member;                    // [kGB] member index inside its group
+  int32_t* tslot;                      // [kGB] resolver slot of each term
+  int32_t* slot_old;                   // [kGB]
+  int32_t* slot_chunks;                // [kGB][kSlotChunks]
+  int32_t* group_of;                   // M (output)
+};
+
+__device__ __forceinline__ int swap_entry(int e, int W) { return e < 64 * W ? e + 64 * W : e - 64 * W; }
+
+// ------------------------------------------------------------ fit tests
+template <int W>
+__device__ bool deep_fit(const GCtx& G, int g, const uint16_t* lst, uint32_t cnt) {
+  constexpr int E = 128 * W;
+  int c = G.gfirst[g];
+  c = c >= 0 ? G.cnext[c] : -1;  // chunk 0 already tested
+  while (c >= 0) {
+    const u64* T = G.pool + (int64_t)c * E;
+    u64 acc = 0;
+    for (uint32_t k = 0; k < cnt; ++k) acc ^= T[lst[k]];
+    if (acc) return false;
+    c = G.cnext[c];
+  }
+  return true;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kGB, 1) k_group_fit(GCtx G, int64_t b0, int bn) {
+  constexpr int E = 128 * W;
+  constexpr int GPC = 8;  // groups per shared-memory pass (8 KB x W)
+  extern __shared__ u64 S[];  // [GPC][E]
+  if (*G.overflow) return;
+  const uint32_t G0 = *G.gcur;
+  const int t = threadIdx.x;
+  const bool valid = t < bn;
+  uint32_t off = 0, cnt = 0;
+  if (valid) {
+    off = G.off[b0 + t];
+    cnt = G.off[b0 + t + 1] - off;
+  }
+  const uint16_t* lst = G.list + off;
+  const int64_t nwords = ((int64_t)G0 + 31) / 32;
+  for (int64_t gw = blockIdx.x; gw < nwords; gw += gridDim.x) {
+    uint32_t word = 0;
+#pragma unroll 1
+    for (int h = 0; h < 32 / GPC; ++h) {
+      const int64_t g0 = gw * 32 + h * GPC;
+      for (int i = threadIdx.x; i < GPC * E; i += blockDim.x) {
+        const int gi = i / E, e = i % E;
+        const int64_t g = g0 + gi;
+        u64 v = 0;
+        if (g < G0) {
+          const int c = G.gfirst[g];
+          v = G.pool[(int64_t)c * E + e];
+        }
+        S[gi * E + e] = v;
+      }
+      __syncthreads();
+      if (valid && g0 < G0) {
+        u64 acc[GPC];
+#pragma unroll
+        for (int q = 0; q < GPC; ++q) acc[q] = 0;
+        for (uint32_t k = 0; k < cnt; ++k) {
+          const int e = lst[k];
+#pragma unroll
+          for (int q = 0; q < GPC; ++q) acc[q] ^= S[q * E + e];
+        }
+        uint32_t cand = 0;
+#pragma unroll
+        for (int q = 0; q < GPC; ++q) cand |= (acc[q] == 0 ? 1u : 0u) << q;
+        for (; cand; cand &= cand - 1) {  // rare: chunk 0 commutes
+          const int q = __ffs(cand) - 1;
+          const int64_t g = g0 + q;
+          if (g < G0 && (G.gsize[g] <= 64 || deep_fit<W>(G, (int)g, lst, cnt)))
+            word |= 1u << (h * GPC + q);
+        }
+      }
+      __syncthreads();
+    }
+    if (valid) G.fit0[(int64_t)t * G.gw_stride + gw] = word;
+  }
+}
+
+// first kGK fitting groups of each batch term (warp per term)
+__global__ void __launch_bounds__(1024) k_group_firstk(GCtx G, int bn) {
+  if (*G.overflow) return;
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (t >= bn) return;
+  const uint32_t G0 = *G.gcur;
+  const int64_t nwords = ((int64_t)G0 + 31) / 32;
+  const uint32_t* row = G.fit0 + (int64_t)t * G.gw_stride;
+  int found = 0;
+  int32_t mine = -1;
+  for (int64_t base = 0; base < nwords && found <= kGK; base += 32) {
+    const int64_t w = base + lane;
+    uint32_t v = w < nwords ? row[w] : 0u;
+    unsigned nz = __ballot_sync(0xffffffffu, v != 0);
+    while (nz && found <= kGK) {
+      const int src = __ffs(nz) - 1;
+      nz &= nz - 1;
+      uint32_t bits = __shfl_sync(0xffffffffu, v, src);
+      while (bits && found <= kGK) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        if (found < kGK && lane == found) mine = (int32_t)((base + src) * 32 + b);
+        ++found;
+      }
+    }
+  }
+  if (lane < kGK) G.fitk[t * kGK + lane] = mine;
+  if (lane == 0) G.nfit[t] = found;  // kGK + 1 means "more than kGK"
+}
+
+// ------------------------------------------------------------ resolver
+struct ResolveSmem {
+  int32_t hkey[kHash];
+  int32_t hval[kHash];
+  int32_t slot_group[kGB];
+  int32_t slot_old[kGB];
+  int32_t slot_cnt[kGB];
+  int32_t newg[kGB];
+  uint32_t mask[kGB][kGAW];
+};
+
+__device__ __forceinline__ int hfind(const ResolveSmem& R, int g) {
+  int h = (int)(((unsigned)g * 2654435761u) >> 21) & (kHash - 1);
+  for (;;) {
+    const int k = R.hkey[h];
+    if (k == g) return R.hval[h];
+    if (k < 0) return -1;
+    h = (h + 1) & (kHash - 1);
+  }
+}
+
+__device__ __forceinline__ void hinsert(ResolveSmem& R, int g, int s) {
+  int h = (int)(((unsigned)g * 2654435761u) >> 21) & (kHash - 1);
+  while (R.hkey[h] >= 0) h = (h + 1) & (kHash - 1);
+  R.hkey[h] = g;
+  R.hval[h] = s;
+}
+
+__global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int bn) {
+  extern __shared__ uint8_t smraw[];
+  ResolveSmem& R = *reinterpret_cast<ResolveSmem*>(smraw);
+  if (*G.overflow) return;
+  const int lane = threadIdx.x;
+  for (int i = lane; i < kHash; i += 32) R.hkey[i] = -1;
+  __syncwarp();
+  const uint32_t G0 = *G.gcur;
+  uint32_t gcur = G0;
+  int nslots = 0, nnew = 0;
+  bool ovf = false;
+  for (int i = 0; i < bn && !ovf; ++i) {
+    // anti-commutation with earlier batch terms only (u < i)
+    uint32_t aw = G.anti[(int64_t)i * kGAW + lane];
+    const int wi = i >> 5;
+    aw = lane < wi ? aw : (lane == wi ? (aw & ((1u << (i & 31)) - 1u)) : 0u);
+    const int nf = G.nfit[i];
+    const int32_t fk = lane < kGK ? G.fitk[i * kGK + lane] : -1;
+    int chosen = -1;
+    const int ncand = nf < kGK ? nf : kGK;
+    for (int k = 0; k < ncand && chosen < 0; ++k) {
+      const int c = __shfl_sync(0xffffffffu, fk, k);
+      const int s = hfind(R, c);
+      if (s < 0 || !__any_sync(0xffffffffu, (aw & R.mask[s][lane]) != 0u)) chosen = c;
+    }
+    if (chosen < 0 && nf > kGK) {  // rare: all first-k candidates blocked
+      const int64_t nwords = ((int64_t)G0 + 31) / 32;
+      const uint32_t* row = G.fit0 + (int64_t)i * G.gw_stride;
+      const int last = __shfl_sync(0xffffffffu, fk, kGK - 1);
+      for (int64_t w = (last + 1) / 32; w < nwords && chosen < 0; ++w) {
+        uint32_t bits = row[w];
+        if (w == (last + 1) / 32) bits &= ~((1u << ((last + 1) & 31)) - 1u);
+        while (bits && chosen < 0) {
+          const int c = (int)(w * 32) + __ffs(bits) - 1;
+          bits &= bits - 1;
+          const int s = hfind(R, c);
+          if (s < 0 || !__any_sync(0xffffffffu, (aw & R.mask[s][lane]) != 0u)) chosen = c;
+        }
+      }
+    }
+    if (chosen < 0) {  // groups opened earlier in this batch, creation order
+      for (int k = 0; k < nnew && chosen < 0; ++k) {
+        const int s = R.newg[k];
+        if (!__any_sync(0xffffffffu, (aw & R.mask[s][lane]) != 0u)) chosen = R.slot_group[s];
+      }
+    }
+    int s;
+    if (chosen < 0) {
+      if ((int64_t)gcur >= G.gcap) {
+        ovf = true;
+        break;
+      }
+      chosen = (int)gcur++;
+      s = nslots++;
+      if (lane == 0) {
+        R.slot_group[s] = chosen;
+        R.slot_old[s] = 0;
+        R.slot_cnt[s] = 0;
+        R.newg[nnew] = s;
+        hinsert(R, chosen, s);
+      }
+      R.mask[s][lane] = 0u;
+      ++nnew;
+    } else {
+      s = hfind(R, chosen);
+      if (s < 0) {
+        s = nslots++;
+        if (lane == 0) {
+          R.slot_group[s] = chosen;
+          R.slot_old[s] = (int32_t)G.gsize[chosen];
+          R.slot_cnt[s] = 0;
+          hinsert(R, chosen, s);
+        }
+        R.mask[s][lane] = 0u;
+      }
+    }
+    __syncwarp();
+    if (lane == wi) R.mask[s][lane] |= 1u << (i & 31);
+    if (lane == 0) {
+      G.group_of[b0 + i] = chosen;
+      G.member[i] = (uint32_t)(R.slot_old[s] + R.slot_cnt[s]);
+      G.tslot[i] = s;
+      R.slot_cnt[s] += 1;
+    }
+    __syncwarp();
+  }
+  if (ovf) {
+    if (lane == 0) *G.overflow = 1;
+    return;
+  }
+  // grow every touched group: allocate chunks, link, record chunk tables
+  for (int s = lane; s < nslots; s += 32) {
+    const int g = R.slot_group[s];
+    const int old = R.slot_old[s], nw = old + R.slot_cnt[s];
+    const int have = (old + 63) / 64, need = (nw + 63) / 64;
+    const int add = need - have;
+    int base = 0;
+    if (add > 0) base = (int)atomicAdd(G.pool_next, (uint32_t)add);
+    if ((int64_t)base + add > G.ccap) {
+      *G.overflow = 1;
+      continue;
+    }
+    int prev = have > 0 ? G.glast[g] : -1;
+    int32_t* tab = G.slot_chunks + (int64_t)s * kSlotChunks;
+    int k = 0;
+    if (old % 64) tab[k++] = prev;  // partially filled last chunk
+    for (int a = 0; a < add; ++a) {
+      const int id = base + a;
+      G.cnext[id] = -1;
+      if (prev < 0) G.gfirst[g] = id;
+      else G.cnext[prev] = id;
+      prev = id;
+      tab[k++] = id;
+    }
+    if (add > 0) G.glast[g] = prev;
+    G.gsize[g] = (uint32_t)nw;
+    G.slot_old[s] = old;
+  }
+  if (lane == 0) *G.gcur = gcur;
+}
+
+// ------------------------------------------------------------ update
+template <int W>
+__global__ void __launch_bounds__(kGB, 1) k_group_update(GCtx G, int64_t b0, int bn,
+                                                         const uint32_t* g0_snap) {
+  constexpr int E = 128 * W;
+  __shared__ int32_t sg[kGB];
+  __shared__ unsigned long long red[32];
+  if (*G.overflow) return;
+  const uint32_t g0_batch = *g0_snap;  // groups that existed at batch start
+  const int i = threadIdx.x;
+  if (i < bn) sg[i] = G.group_of[b0 + i];
+  __syncthreads();
+  unsigned long long chk = 0;
+  if (i < bn) {
+    const int s = G.tslot[i];
+    const uint32_t m = G.member[i];
+    const int old = G.slot_old[s];
+    const int chunk = G.slot_chunks[(int64_t)s * kSlotChunks + (int)(m / 64) - old / 64];
+    const u64 bit = 1ull << (m & 63);
+    const uint32_t off = G.off[b0 + i], cnt = G.off[b0 + i + 1] - off;
+    u64* T = G.pool + (int64_t)chunk * E;
+    for (uint32_t k = 0; k < cnt; ++k) atomicOr(&T[swap_entry(G.list[off + k], W)], bit);
+    // pair_checks: #{u < t : group(u) <= group(t)}
+    const int c = sg[i];
+    chk = (uint32_t)c < g0_batch ? (unsigned long long)G.gpre[c] : (unsigned long long)b0;
+    for (int u = 0; u < i; ++u) chk += sg[u] <= c ? 1ull : 0ull;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) chk += __shfl_xor_sync(0xffffffffu, chk, o);
+  if ((i & 31) == 0) red[i >> 5] = chk;
+  __syncthreads();
+  if (i == 0) {
+    unsigned long long s = 0;
+    for (int w = 0; w < kGB / 32; ++w) s += red[w];
+    atomicAdd(G.checks, s);
+  }
+}
+
+// inclusive prefix of group sizes at batch start (single CTA) + G0 snapshot
+__global__ void __launch_bounds__(1024) k_group_prefix(GCtx G, uint32_t* g0_out) {
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t carry;
+  if (*G.overflow) return;
+  const uint32_t G0 = *G.gcur;
+  if (threadIdx.x == 0) {
+    carry = 0;
+    *g0_out = G0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint32_t base = 0; base < G0; base += blockDim.x) {
+    const uint32_t g = base + threadIdx.x;
+    const uint32_t v = g < G0 ? G.gsize[g] : 0u;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    uint32_t before = 0, tot = 0;
+    for (int w = 0; w < 32; ++w) {
+      before += w < wid ? wsum[w] : 0u;
+      tot += wsum[w];
+    }
+    if (g < G0) G.gpre[g] = carry + before + inc;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ host side
+static inline int64_t a256(int64_t v) { return (v + 255) & ~(int64_t)255; }
+
+struct GLayout {
+  int64_t off, scratch, fixed_end;  // after fixed_end: list | groups | pool
+};
+
+static int64_t per_group_bytes(int W, int64_t gw_stride_per_group) {
+  (void)gw_stride_per_group;
+  return 4 * 4 /* gsize gfirst glast gpre */ + kGB / 8 /* fit0 bits */ +
+         (128LL * W * 8 + 4) /* one chunk */;
+}
+
+static int64_t fixed_bytes(int W, int64_t M) {
+  (void)W;
+  int64_t o = 0;
+  o += a256((M + 1) * 4);                       // off
+  o += a256(scan_scratch_words(M) * 4);         // scan scratch
+  o += a256(64);                                // scalars
+  o += a256((int64_t)kGB * kGK * 4) + a256(kGB * 4) + a256((int64_t)kGB * kGAW * 4);
+  o += a256(kGB * 4) * 3 + a256((int64_t)kGB * kSlotChunks * 4);
+  o += a256(16);                                // g0 snapshot
+  return o;
+}
+
+template <int W>
+static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t* group_of,
+                     int32_t* n_groups, int64_t* pair_checks, void* ws, size_t ws_bytes,
+                     cudaStream_t st) {
+  uint8_t* b = (uint8_t*)ws;
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) {
+    uint8_t* p = b + o;
+    o = a256(o + bytes);
+    return p;
+  };
+  GCtx G{};
+  G.W = W;
+  G.M = M;
+  G.x = x;
+  G.z = z;
+  G.ld = ld;
+  uint32_t* off = (uint32_t*)take((M + 1) * 4);
+  uint32_t* scratch = (uint32_t*)take(scan_scratch_words(M) * 4);
+  uint32_t* scal = (uint32_t*)take(64);
+  G.fitk = (int32_t*)take((int64_t)kGB * kGK * 4);
+  G.nfit = (int32_t*)take(kGB * 4);
+  G.anti = (uint32_t*)take((int64_t)kGB * kGAW * 4);
+  G.member = (uint32_t*)take(kGB * 4);
+  G.tslot = (int32_t*)take(kGB * 4);
+  G.slot_old = (int32_t*)take(kGB * 4);
+  G.slot_chunks = (int32_t*)take((int64_t)kGB * kSlotChunks * 4);
+  uint32_t* g0snap = (uint32_t*)take(16);
+  if (o > (int64_t)ws_bytes) {
+    set_error("pl_group_greedy: workspace too small");
+    return PL_ERR_WORKSPACE;
+  }
+  PLB_CUDA(cudaMemsetAsync(scal, 0, 64, st));
+  G.gcur = scal;
+  G.pool_next = scal + 1;
+  G.overflow = scal + 2;
+  G.checks = (unsigned long long*)(scal + 4);
+  // CSR entry lists of every term (same encoding as the bitmatrix)
+  const unsigned nb = (unsigned)ceil_div(M, 256);
+  {
+    StageTimer t_(st, "k_row_weight");
+    k_row_weight<W><<<nb, 256, 0, st>>>(x, z, ld, 0, M, off);
+    PLB_CHECK_LAUNCH("k_row_weight");
+  }
+  int rc = exclusive_scan_u32(off, off, M, scratch, off + M, st);
+  if (rc) return rc;
+  uint32_t total = 0;
+  PLB_CUDA(cudaMemcpyAsync(&total, off + M, 4, cudaMemcpyDeviceToHost, st));
+  PLB_CUDA(cudaStreamSynchronize(st));
+  uint16_t* list = (uint16_t*)take((int64_t)total * 2 + 16);
+  G.off = off;
+  G.list = list;
+  // remaining bytes -> group capacity
+  const int64_t rest = (int64_t)ws_bytes - o - 4096;
+  const int64_t chunk_bytes = 128LL * W * 8 + 4;
+  const int64_t member_chunks = (M + 63) / 64;
+  int64_t gcap = (rest - member_chunks * chunk_bytes) / per_group_bytes(W, 0);
+  if (gcap > M) gcap = M;
+  if (gcap < 1) {
+    set_error("pl_group_greedy: workspace too small for the entry lists (%u entries)", total);
+    return PL_ERR_WORKSPACE;
+  }
+  G.gcap = gcap;
+  G.ccap = gcap + member_chunks;
+  G.gw_stride = (gcap + 31) / 32;
+  G.gsize = (uint32_t*)take(gcap * 4);
+  G.gfirst = (int32_t*)take(gcap * 4);
+  G.glast = (int32_t*)take(gcap * 4);
+  G.gpre = (uint32_t*)take(gcap * 4);
+  G.fit0 = (uint32_t*)take((int64_t)kGB * G.gw_stride * 4);
+  G.cnext = (int32_t*)take(G.ccap * 4);
+  G.pool = (u64*)take(G.ccap * 128LL * W * 8);
+  if (o > (int64_t)ws_bytes) {
+    set_error("pl_group_greedy: workspace layout overflow");
+    return PL_ERR_WORKSPACE;
+  }
+  PLB_CUDA(cudaMemsetAsync(G.gsize, 0, gcap * 4, st));
+  PLB_CUDA(cudaMemsetAsync(G.pool, 0, G.ccap * 128LL * W * 8, st));
+  G.group_of = group_of;
+  {
+    StageTimer t_(st, "k_row_fill");
+    k_row_fill<W><<<nb, 256, 0, st>>>(x, z, ld, 0, M, off, list);
+    PLB_CHECK_LAUNCH("k_row_fill");
+  }
+  const size_t fit_smem = (size_t)8 * 128 * W * 8;
+  PLB_CUDA(cudaFuncSetAttribute(k_group_fit<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)fit_smem));
+  PLB_CUDA(cudaFuncSetAttribute(k_group_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(ResolveSmem)));
+  const size_t lists_smem = (size_t)32 * (128 * W + kTPad) * 4;
+  if (W <= 8) {
+    PLB_CUDA(cudaFuncSetAttribute(k_bitmatrix_lists<W>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lists_smem));
+  }
+  const int fit_grid = 2 * num_sms();
+  for (int64_t b0 = 0; b0 < M; b0 += kGB) {
+    const int bn = (int)std::min<int64_t>(kGB, M - b0);
+    {
+      StageTimer t_(st, "k_group_prefix");
+      k_group_prefix<<<1, 1024, 0, st>>>(G, g0snap);
+    }
+    {
+      StageTimer t_(st, "k_group_anti");
+      if (W <= 8) {
+        dim3 grid(1, (unsigned)ceil_div(bn, 256));
+        k_bitmatrix_lists<W><<<grid, 1024, lists_smem, st>>>(x, z, ld, M, b0, bn, b0, bn,
+                                                             off + b0, list, G.anti, kGAW, 256);
+      } else {
+        constexpr int kDC = DirectCols<W>::value;
+        dim3 grid((unsigned)ceil_div(bn, kDC), (unsigned)ceil_div(bn, kDirectRows));
+        k_bitmatrix_direct<W><<<grid, kDirectRows, 0, st>>>(x, z, ld, M, b0, bn, b0, bn, G.anti,
+                                                            kGAW);
+      }
+    }
+    if (b0 > 0) {
+      StageTimer t_(st, "k_group_fit");
+      k_group_fit<W><<<fit_grid, kGB, fit_smem, st>>>(G, b0, bn);
+    }
+    {
+      StageTimer t_(st, "k_group_firstk");
+      if (b0 > 0) k_group_firstk<<<kGB / 32, 1024, 0, st>>>(G, bn);
+      else PLB_CUDA(cudaMemsetAsync(G.nfit, 0, kGB * 4, st));
+    }
+    {
+      StageTimer t_(st, "k_group_resolve");
+      k_group_resolve<<<1, 32, sizeof(ResolveSmem), st>>>(G, b0, bn);
+    }
+    {
+      StageTimer t_(st, "k_group_update");
+      k_group_update<W><<<1, kGB, 0, st>>>(G, b0, bn, g0snap);
+    }
+    PLB_CHECK_LAUNCH("grouping batch");
+  }
+  uint32_t ovf = 0;
+  PLB_CUDA(cudaMemcpyAsync(&ovf, G.overflow, 4, cudaMemcpyDeviceToHost, st));
+  PLB_CUDA(cudaMemcpyAsync(n_groups, G.gcur, 4, cudaMemcpyDeviceToDevice, st));
+  PLB_CUDA(cudaMemcpyAsync(pair_checks, G.checks, 8, cudaMemcpyDeviceToDevice, st));
+  PLB_CUDA(cudaStreamSynchronize(st));
+  if (ovf) {
+    set_error("pl_group_greedy: group capacity %lld exceeded; pass a larger workspace",
+              (long long)gcap);
+    return PL_ERR_WORKSPACE;
+  }
+  return PL_OK;
+}
+
+}  // namespace plb
+
 using namespace plb;
-extern "C" int64_t pl_group_workspace_bytes(int, int64_t) { return 0; }
-extern "C" int pl_group_greedy(int, int64_t, const uint64_t*, const uint64_t*, int64_t, int32_t*,
-                               int32_t*, int64_t*, void*, size_t, void*) {
-  set_error("pl_group_greedy: not implemented yet");
-  return PL_ERR_ARG;
+
+extern "C" int64_t pl_group_workspace_bytes(int W, int64_t M) {
+  if (M <= 0 || !valid_words(W)) return 4096;
+  // recommended: entry lists for ~24 set bits per term and groups for M/8
+  const int64_t lists = M * 48 + 16;
+  int64_t groups = M / 8;
+  if (groups < 1024) groups = std::min<int64_t>(M, 1024);
+  const int64_t chunks = (M + 63) / 64;
+  return fixed_bytes(W, M) + a256(lists) + groups * per_group_bytes(W, 0) +
+         chunks * (128LL * W * 8 + 4) + 64 * 256;
+}
+
+extern "C" int pl_group_greedy(int W, int64_t M, const uint64_t* x, const uint64_t* z,
+                               int64_t ld, int32_t* group_of, int32_t* n_groups,
+                               int64_t* pair_checks, void* workspace, size_t workspace_bytes,
+                               void* stream) {
+  if (M < 0 || ld < M || !group_of || !n_groups || !pair_checks) {
+    set_error("pl_group_greedy: bad arguments");
+    return PL_ERR_ARG;
+  }
+  if (M * 128LL * (W > 0 ? W : 1) >= 0xFFFFFFFFLL || M >= (1LL << 31)) {
+    set_error("pl_group_greedy: too many terms for 32-bit entry offsets");
+    return PL_ERR_CAPACITY;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (M == 0) {
+    PLB_CUDA(cudaMemsetAsync(n_groups, 0, 4, st));
+    PLB_CUDA(cudaMemsetAsync(pair_checks, 0, 8, st));
+    return PL_OK;
+  }
+  return PLB_DISPATCH_W(W, run_group, M, (const u64*)x, (const u64*)z, ld, group_of, n_groups,
+                        pair_checks, workspace, workspace_bytes, st);
 }

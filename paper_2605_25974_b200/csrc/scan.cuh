@@ -40,7 +40,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total)
   return before + inc - v;
 }
 
-__global__ void k_scan_block_sums(const uint32_t* __restrict__ in, int64_t n,
+static __global__ void k_scan_block_sums(const uint32_t* __restrict__ in, int64_t n,
                                   uint32_t* __restrict__ block_sums) {
   const int64_t base = (int64_t)blockIdx.x * kScanTile;
   uint32_t s = 0;
@@ -55,7 +55,7 @@ __global__ void k_scan_block_sums(const uint32_t* __restrict__ in, int64_t n,
 }
 
 // Single block: exclusive scan of nb block sums in place; total -> *total.
-__global__ void k_scan_partials(uint32_t* __restrict__ sums, int64_t nb, uint32_t* total) {
+static __global__ void k_scan_partials(uint32_t* __restrict__ sums, int64_t nb, uint32_t* total) {
   uint32_t carry = 0;
   for (int64_t base = 0; base < nb; base += blockDim.x) {
     const int64_t i = base + threadIdx.x;
@@ -69,7 +69,7 @@ __global__ void k_scan_partials(uint32_t* __restrict__ sums, int64_t nb, uint32_
 }
 
 // out[i] = exclusive prefix of in[i]; in and out may alias.
-__global__ void k_scan_apply(const uint32_t* in, int64_t n, const uint32_t* __restrict__ block_off,
+static __global__ void k_scan_apply(const uint32_t* in, int64_t n, const uint32_t* __restrict__ block_off,
                              uint32_t* out) {
   const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
   uint32_t v[kScanItems];

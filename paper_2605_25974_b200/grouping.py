@@ -80,11 +80,23 @@ def group_assignment(s: PauliSumSoA):
     pc = torch.zeros(1, dtype=torch.int64, device=dev)
     if M:
         ws_bytes = int(_native.load().pl_group_workspace_bytes(S.W, M))
-        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
-        with torch.cuda.device(dev):
-            _native.call("pl_group_greedy", S.W, M, ptr(S.x), ptr(S.z), S.ld, ptr(gof), ptr(ng),
-                         ptr(pc), ptr(ws), ws.numel(), stream_ptr(dev))
+        lib = _native.load()
+        for _ in range(6):  # grow the workspace if the group/list capacity overflowed
+            ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+            with torch.cuda.device(dev):
+                rc = lib.pl_group_greedy(S.W, M, ptr(S.x), ptr(S.z), S.ld, ptr(gof), ptr(ng),
+                                         ptr(pc), ptr(ws), ws.numel(), stream_ptr(dev))
+            if rc != _PL_ERR_WORKSPACE:
+                _native.check(rc, "pl_group_greedy")
+                break
+            del ws
+            ws_bytes *= 4
+        else:
+            _native.check(rc, "pl_group_greedy")
     return gof[:M], ng, pc
+
+
+_PL_ERR_WORKSPACE = -5
 
 
 def group_greedy(s, *, stats: GroupingStats | None = None) -> CommutationPartition:
