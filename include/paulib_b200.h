@@ -130,6 +130,42 @@ int pl_outer_multiply_combine(const pl_merge_plan* plan,
                               uint64_t* ox, uint64_t* oz, uint8_t* ok, double* oc, int64_t ldo,
                               int64_t* out_count, void* stream);
 
+/* ------------------------------------------------------------------------
+ * K7 — multi-GPU A*B (no reference equivalent; PAPER.md:712-714 lists
+ * distributed memory as future work).  Every rank builds the same plan from
+ * the replicated A and B, so the key-range splitters (from a deterministic
+ * sample of the full product) are identical everywhere without a collective.
+ *   1. pl_outer_partition: rank r generates the items of B columns [j0, j1),
+ *      buckets them, writes them bucket-contiguous into `send` as records of
+ *      pl_dist_item_bytes() bytes and the per-bucket counts (n_buckets u32,
+ *      device) into bucket_counts;
+ *   2. the caller exchanges bucket ranges (rank q owns buckets [b0_q, b1_q))
+ *      with one all-to-all (NCCL, see paper_2605_25974_b200/dist.py);
+ *   3. pl_merge_received: merge the received records (source-major; counts is
+ *      the device [n_ranks][b1-b0] matrix of per-source, per-bucket counts)
+ *      into this rank's slice of the canonical output.
+ * Concatenating the ranks' outputs in rank order gives exactly the
+ * single-GPU pl_outer_multiply_combine result (runs never straddle buckets,
+ * each run is summed in raw-row order by one thread).
+ */
+int pl_dist_item_bytes(const pl_merge_plan* plan);
+int64_t pl_dist_workspace_bytes(const pl_merge_plan* plan, int64_t n_local,
+                                int32_t n_buckets_local);
+int pl_outer_partition(const pl_merge_plan* plan,
+                       const uint64_t* ax, const uint64_t* az, const uint8_t* ak, int64_t lda,
+                       const uint64_t* bx, const uint64_t* bz, const uint8_t* bk, int64_t ldb,
+                       int64_t j0, int64_t j1, void* workspace, size_t workspace_bytes,
+                       void* send, uint32_t* bucket_counts, void* stream);
+int pl_merge_received(const pl_merge_plan* plan, const void* recv, int64_t n_recv,
+                      const uint32_t* counts, int n_ranks, int32_t b0, int32_t b1,
+                      const uint64_t* ax, const uint64_t* az, const uint8_t* ak,
+                      const double* ac, int64_t lda,
+                      const uint64_t* bx, const uint64_t* bz, const uint8_t* bk,
+                      const double* bc, int64_t ldb,
+                      double eps, void* workspace, size_t workspace_bytes,
+                      uint64_t* ox, uint64_t* oz, uint8_t* ok, double* oc, int64_t ldo,
+                      int64_t* out_count, void* stream);
+
 /* sort_and_combine (sums.py:286-291 / :94-120) of one sum. */
 int pl_sort_combine(const pl_merge_plan* plan,
                     const uint64_t* x, const uint64_t* z, const uint8_t* k, const double* c,

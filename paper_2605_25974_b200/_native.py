@@ -70,6 +70,13 @@ SIGNATURES = {
     "pl_bitmatrix_workspace_bytes": (_L, [_I, _L]),
     "pl_group_workspace_bytes": (_L, [_I, _L]),
     "pl_group_greedy": (_I, [_I, _L, _P, _P, _L, _P, _P, _P, _P, _S, _P]),
+    "pl_dist_item_bytes": (_I, [C.POINTER(MergePlan)]),
+    "pl_dist_workspace_bytes": (_L, [C.POINTER(MergePlan), _L, C.c_int32]),
+    "pl_outer_partition": (_I, [C.POINTER(MergePlan), _P, _P, _P, _L, _P, _P, _P, _L, _L, _L,
+                                _P, _S, _P, _P, _P]),
+    "pl_merge_received": (_I, [C.POINTER(MergePlan), _P, _L, _P, _I, C.c_int32, C.c_int32,
+                               _P, _P, _P, _P, _L, _P, _P, _P, _P, _L, _D, _P, _S,
+                               _P, _P, _P, _P, _L, _P, _P]),
     "pl_stage_timing": (_I, [_I]),
     "pl_stage_times": (_I, [_P, _P, _I]),
 }

@@ -67,7 +67,8 @@ struct Ctl {  // control arrays inside the workspace
 };
 
 struct Dims {
-  int64_t n, ma, mb;
+  int64_t n, ma, mb;     // items held here; |A|; B columns generated here
+  int64_t n_space, j0;   // full raw-product size (sampling space); first B column
   int nb1, nsamp, leaf_cap, leaf_target, max_sub, max_leaves;
 };
 
@@ -386,7 +387,7 @@ k_sample(Layout L, Dims D, SrcA S, Ctl C) {
   u64* K = sm;
   uint32_t* I = reinterpret_cast<uint32_t*>(K + (int64_t)KW * ns);
   for (int s = threadIdx.x; s < ns; s += blockDim.x) {
-    const int64_t r = ((2 * (int64_t)s + 1) * D.n) / (2 * (int64_t)ns);
+    const int64_t r = ((2 * (int64_t)s + 1) * D.n_space) / (2 * (int64_t)ns);
     u64 key[KW];
     int k;
     Source<W, KW, MODE>::item_at(L, S, D.ma, r, key, k);
@@ -448,14 +449,15 @@ struct Gen {
     if (MODE == 0) {
       i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
       valid_i = i < D.ma;
-      const int64_t j0 = (int64_t)blockIdx.y * kGenTB;
+      const int64_t j0 = D.j0 + (int64_t)blockIdx.y * kGenTB;
       // b tile into shared memory (z words then x words)
       for (int t = threadIdx.x; t < 2 * W * kGenTB; t += blockDim.x) {
         const int s = t / kGenTB, jj = t % kGenTB;
         const int w = s < W ? s : s - W;
         const int64_t j = j0 + jj;
         u64 v = 0;
-        if (j < D.mb && (L.active >> w & 1)) v = s < W ? S.bz[w * S.ldb + j] : S.bx[w * S.ldb + j];
+        if (j < D.j0 + D.mb && (L.active >> w & 1))
+          v = s < W ? S.bz[w * S.ldb + j] : S.bx[w * S.ldb + j];
         g.tile[s * kGenTB + jj] = v;
       }
       ka = 0;
@@ -476,8 +478,8 @@ struct Gen {
     int64_t r;
     int k;
     if (MODE == 0) {
-      const int64_t j = (int64_t)blockIdx.y * kGenTB + jj;
-      if (!valid_i || j >= D.mb) return false;
+      const int64_t j = D.j0 + (int64_t)blockIdx.y * kGenTB + jj;  // global B index
+      if (!valid_i || j >= D.j0 + D.mb) return false;
       k = ka + (S.bk ? S.bk[j] : 0);
 #pragma unroll
       for (int w = 0; w < W; ++w) {
@@ -1009,6 +1011,192 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const O
   return PL_OK;
 }
 
+// ------------------------------------------------------ K7 multi-GPU stages
+// Record layout exchanged between ranks: KW key words then ik, (KW+1) u64.
+template <int KW>
+__global__ void k_pack(const Ctl C, int64_t n, u64* __restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int d = 0; d < KW; ++d) out[t * (KW + 1) + d] = C.k1[d * n + t];
+    out[t * (KW + 1) + KW] = C.i1[t];
+  }
+}
+
+// counts [G][nbl] -> bucket totals, per-segment source offsets and
+// destination offsets inside the bucket (one CTA, nbl <= kMaxBuckets)
+__global__ void __launch_bounds__(1024)
+k_regroup_prep(const uint32_t* __restrict__ cnt, int G, int nbl, Ctl C, uint32_t* seg_src,
+               uint32_t* seg_dst) {
+  __shared__ uint32_t src_base[65];
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0;
+    for (int s = 0; s < G; ++s) {
+      src_base[s] = acc;
+      for (int b = 0; b < nbl; ++b) acc += cnt[s * nbl + b];
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbl; b += blockDim.x) {
+    uint32_t in_bucket = 0;
+    for (int s = 0; s < G; ++s) {
+      seg_dst[s * nbl + b] = in_bucket;
+      in_bucket += cnt[s * nbl + b];
+    }
+    C.bcount[b] = in_bucket;
+  }
+  if (threadIdx.x < G) {
+    const int s = threadIdx.x;
+    uint32_t acc = src_base[s];
+    for (int b = 0; b < nbl; ++b) {
+      seg_src[s * nbl + b] = acc;
+      acc += cnt[s * nbl + b];
+    }
+  }
+}
+
+template <int KW>
+__global__ void k_regroup_copy(const u64* __restrict__ recv, const uint32_t* __restrict__ cnt,
+                               int nbl, const uint32_t* __restrict__ seg_src,
+                               const uint32_t* __restrict__ seg_dst, Ctl C, int64_t n) {
+  const int b = blockIdx.x, s = blockIdx.y;
+  const uint32_t c = cnt[s * nbl + b];
+  const uint64_t src = seg_src[s * nbl + b];
+  const uint64_t dst = (uint64_t)C.bbase[b] + seg_dst[s * nbl + b];
+  for (uint32_t t = threadIdx.x; t < c; t += blockDim.x) {
+    const u64* r = recv + (src + t) * (KW + 1);
+#pragma unroll
+    for (int d = 0; d < KW; ++d) C.k1[d * n + dst + t] = r[d];
+    C.i1[dst + t] = (uint32_t)r[KW];
+  }
+}
+
+static pl_merge_plan local_plan(const pl_merge_plan& P, int64_t n_local, int nb) {
+  pl_merge_plan Q = P;
+  Q.n_items = n_local;
+  Q.n_buckets = nb;
+  Q.workspace_bytes = ws_layout(Q).total + align256(8LL * 64 * nb);
+  return Q;
+}
+
+template <int W, int KW>
+static int run_partition(const pl_merge_plan& P, const SrcA& S, int64_t j0, int64_t j1, void* ws,
+                         void* send, uint32_t* counts_out, cudaStream_t st) {
+  const pl_merge_plan Q = local_plan(P, P.ma * (j1 - j0), P.n_buckets);
+  const Layout L = to_layout(Q);
+  Dims D = to_dims(Q);
+  D.n_space = P.n_items;
+  D.mb = j1 - j0;
+  D.j0 = j0;
+  const Ctl C = to_ctl(Q, ws);
+  const WsLayout wl = ws_layout(Q);
+  PLB_CUDA(cudaMemsetAsync(ws, 0, (size_t)wl.leaf_desc, st));
+  if (D.n > 0) {
+    if (D.nb1 > 1) {
+      const size_t sm1 = (size_t)D.nsamp * (8 * KW + 4) + 16;
+      if (set_smem(k_sample<W, KW, 0>, sm1)) return PL_ERR_CUDA;
+      StageTimer t_(st, "k_sample");
+      k_sample<W, KW, 0><<<1, kLeafThreads, sm1, st>>>(L, D, S, C);
+      PLB_CHECK_LAUNCH("k_sample");
+    }
+    const size_t gsm = (size_t)8 * KW * D.nb1 + 8 * D.nb1 + 8 + (size_t)16 * W * kGenTB +
+                       (size_t)4 * kGenTB * kGenThreads + 64;
+    const dim3 ggrid((unsigned)ceil_div(D.ma, kGenThreads), (unsigned)ceil_div(D.mb, kGenTB));
+    if (D.nb1 > 1) {
+      if (set_smem(k_count<W, KW, 0>, gsm)) return PL_ERR_CUDA;
+      StageTimer t_(st, "k_count");
+      k_count<W, KW, 0><<<ggrid, kGenThreads, gsm, st>>>(L, D, S, C);
+      PLB_CHECK_LAUNCH("k_count");
+    }
+    {
+      StageTimer t_(st, "k_buckets");
+      k_buckets<<<1, 1024, 0, st>>>(D, C, (int64_t*)(C.n_leaves + 2));
+      PLB_CHECK_LAUNCH("k_buckets");
+    }
+    if (set_smem(k_scatter<W, KW, 0>, gsm)) return PL_ERR_CUDA;
+    {
+      StageTimer t_(st, "k_scatter");
+      k_scatter<W, KW, 0><<<ggrid, kGenThreads, gsm, st>>>(L, D, S, C);
+      PLB_CHECK_LAUNCH("k_scatter");
+    }
+    StageTimer t_(st, "k_pack");
+    k_pack<KW><<<4 * num_sms(), 256, 0, st>>>(C, D.n, (u64*)send);
+    PLB_CHECK_LAUNCH("k_pack");
+  }
+  PLB_CUDA(cudaMemcpyAsync(counts_out, C.bcount, 4 * (size_t)D.nb1, cudaMemcpyDeviceToDevice, st));
+  return PL_OK;
+}
+
+template <int W, int KW>
+static int run_merge_received(const pl_merge_plan& P, const u64* recv, int64_t n_recv,
+                              const uint32_t* cnt, int G, int nbl, const SrcA& S, void* ws,
+                              const OutP& O, cudaStream_t st) {
+  const pl_merge_plan Q = local_plan(P, n_recv, nbl);
+  const Layout L = to_layout(Q);
+  Dims D = to_dims(Q);
+  D.n_space = P.n_items;
+  const Ctl C = to_ctl(Q, ws);
+  const WsLayout wl = ws_layout(Q);
+  uint32_t* seg_src = (uint32_t*)((uint8_t*)ws + wl.total);
+  uint32_t* seg_dst = seg_src + 64 * nbl;
+  PLB_CUDA(cudaMemsetAsync(ws, 0, (size_t)wl.leaf_desc, st));
+  PLB_CUDA(cudaMemsetAsync(O.count, 0, sizeof(int64_t), st));
+  if (n_recv == 0) return PL_OK;
+  {
+    StageTimer t_(st, "k_regroup");
+    k_regroup_prep<<<1, 1024, 0, st>>>(cnt, G, nbl, C, seg_src, seg_dst);
+    PLB_CHECK_LAUNCH("k_regroup_prep");
+    k_buckets<<<1, 1024, 0, st>>>(D, C, O.count);
+    PLB_CHECK_LAUNCH("k_buckets");
+    k_regroup_copy<KW><<<dim3((unsigned)nbl, (unsigned)G), 256, 0, st>>>(recv, cnt, nbl, seg_src,
+                                                                        seg_dst, C, n_recv);
+    PLB_CHECK_LAUNCH("k_regroup_copy");
+  }
+  const int s2cap = (int)P.reserved[1];
+  const size_t ssm = (size_t)s2cap * (8 * KW + 4) + 8 + (size_t)8 * KW * D.max_sub +
+                     (size_t)8 * D.max_sub + 64;
+  if (set_smem(k_split<KW>, ssm)) return PL_ERR_CUDA;
+  {
+    StageTimer t_(st, "k_split");
+    k_split<KW><<<D.nb1, kSplitThreads, ssm, st>>>(D, C, s2cap);
+    PLB_CHECK_LAUNCH("k_split");
+  }
+  const size_t lsm = leaf_smem_bytes(KW);
+  auto lk = k_leaves<W, KW, 0>;
+  if (set_smem(lk, lsm)) return PL_ERR_CUDA;
+  StageTimer t_(st, "k_leaves");
+  lk<<<4 * num_sms(), kLeafThreads2, lsm, st>>>(L, D, S, C, O);
+  PLB_CHECK_LAUNCH("k_leaves");
+  return PL_OK;
+}
+
+template <int W>
+static int dispatch_partition(const pl_merge_plan& P, const SrcA& S, int64_t j0, int64_t j1,
+                              void* ws, void* send, uint32_t* counts, cudaStream_t st) {
+  switch (P.key_words) {
+    case 1: return run_partition<W, 1>(P, S, j0, j1, ws, send, counts, st);
+    case 2: return run_partition<W, 2>(P, S, j0, j1, ws, send, counts, st);
+    case 4: return run_partition<W, (W >= 2 ? 4 : 1)>(P, S, j0, j1, ws, send, counts, st);
+    case 8: return run_partition<W, (W >= 4 ? 8 : 1)>(P, S, j0, j1, ws, send, counts, st);
+    case 16: return run_partition<W, (W >= 8 ? 16 : 1)>(P, S, j0, j1, ws, send, counts, st);
+    default: return run_partition<W, (W >= 16 ? 32 : 1)>(P, S, j0, j1, ws, send, counts, st);
+  }
+}
+
+template <int W>
+static int dispatch_received(const pl_merge_plan& P, const u64* recv, int64_t n_recv,
+                             const uint32_t* cnt, int G, int nbl, const SrcA& S, void* ws,
+                             const OutP& O, cudaStream_t st) {
+  switch (P.key_words) {
+    case 1: return run_merge_received<W, 1>(P, recv, n_recv, cnt, G, nbl, S, ws, O, st);
+    case 2: return run_merge_received<W, 2>(P, recv, n_recv, cnt, G, nbl, S, ws, O, st);
+    case 4: return run_merge_received<W, (W >= 2 ? 4 : 1)>(P, recv, n_recv, cnt, G, nbl, S, ws, O, st);
+    case 8: return run_merge_received<W, (W >= 4 ? 8 : 1)>(P, recv, n_recv, cnt, G, nbl, S, ws, O, st);
+    case 16: return run_merge_received<W, (W >= 8 ? 16 : 1)>(P, recv, n_recv, cnt, G, nbl, S, ws, O, st);
+    default: return run_merge_received<W, (W >= 16 ? 32 : 1)>(P, recv, n_recv, cnt, G, nbl, S, ws, O, st);
+  }
+}
+
 template <int W, int MODE>
 static int dispatch_kw(const pl_merge_plan& P, const SrcA& S, void* ws, const OutP& O,
                        cudaStream_t st) {
@@ -1147,4 +1335,63 @@ extern "C" int pl_sort_combine(const pl_merge_plan* plan, const uint64_t* x, con
          nullptr, nullptr, nullptr, nullptr, 0};
   OutP O{(u64*)ox, (u64*)oz, ok, (double2*)oc, ldo, out_count, eps};
   return PLB_DISPATCH_W(plan->W, run_sort, *plan, S, workspace, O, st);
+}
+
+// ------------------------------------------------------------ K7 C ABI
+extern "C" int pl_dist_item_bytes(const pl_merge_plan* plan) {
+  return plan ? 8 * (plan->key_words + 1) : 0;
+}
+
+extern "C" int64_t pl_dist_workspace_bytes(const pl_merge_plan* plan, int64_t n_local,
+                                           int32_t n_buckets_local) {
+  if (!plan) return 0;
+  return local_plan(*plan, n_local, n_buckets_local > 0 ? n_buckets_local : plan->n_buckets)
+      .workspace_bytes;
+}
+
+extern "C" int pl_outer_partition(const pl_merge_plan* plan, const uint64_t* ax,
+                                  const uint64_t* az, const uint8_t* ak, int64_t lda,
+                                  const uint64_t* bx, const uint64_t* bz, const uint8_t* bk,
+                                  int64_t ldb, int64_t j0, int64_t j1, void* workspace,
+                                  size_t workspace_bytes, void* send, uint32_t* bucket_counts,
+                                  void* stream) {
+  if (!plan || plan->mode != 0 || j0 < 0 || j1 < j0 || j1 > plan->mb || !bucket_counts) {
+    set_error("pl_outer_partition: bad arguments");
+    return PL_ERR_ARG;
+  }
+  const int64_t need = pl_dist_workspace_bytes(plan, plan->ma * (j1 - j0), plan->n_buckets);
+  if ((int64_t)workspace_bytes < need) {
+    set_error("pl_outer_partition: workspace %zu < %lld", workspace_bytes, (long long)need);
+    return PL_ERR_WORKSPACE;
+  }
+  SrcA S{(const u64*)ax, (const u64*)az, ak, nullptr, lda,
+         (const u64*)bx, (const u64*)bz, bk, nullptr, ldb};
+  return PLB_DISPATCH_W(plan->W, dispatch_partition, *plan, S, j0, j1, workspace, send,
+                        bucket_counts, (cudaStream_t)stream);
+}
+
+extern "C" int pl_merge_received(const pl_merge_plan* plan, const void* recv, int64_t n_recv,
+                                 const uint32_t* counts, int n_ranks, int32_t b0, int32_t b1,
+                                 const uint64_t* ax, const uint64_t* az, const uint8_t* ak,
+                                 const double* ac, int64_t lda, const uint64_t* bx,
+                                 const uint64_t* bz, const uint8_t* bk, const double* bc,
+                                 int64_t ldb, double eps, void* workspace, size_t workspace_bytes,
+                                 uint64_t* ox, uint64_t* oz, uint8_t* ok, double* oc, int64_t ldo,
+                                 int64_t* out_count, void* stream) {
+  if (!plan || plan->mode != 0 || n_ranks < 1 || n_ranks > 64 || b0 < 0 || b1 <= b0 ||
+      b1 > plan->n_buckets || n_recv < 0 || ldo < n_recv || eps < 0 || !out_count) {
+    set_error("pl_merge_received: bad arguments");
+    return PL_ERR_ARG;
+  }
+  const int nbl = b1 - b0;
+  const int64_t need = pl_dist_workspace_bytes(plan, n_recv, nbl);
+  if ((int64_t)workspace_bytes < need) {
+    set_error("pl_merge_received: workspace %zu < %lld", workspace_bytes, (long long)need);
+    return PL_ERR_WORKSPACE;
+  }
+  SrcA S{(const u64*)ax, (const u64*)az, ak, (const double2*)ac, lda,
+         (const u64*)bx, (const u64*)bz, bk, (const double2*)bc, ldb};
+  OutP O{(u64*)ox, (u64*)oz, ok, (double2*)oc, ldo, out_count, eps};
+  return PLB_DISPATCH_W(plan->W, dispatch_received, *plan, (const u64*)recv, n_recv, counts,
+                        n_ranks, nbl, S, workspace, O, (cudaStream_t)stream);
 }

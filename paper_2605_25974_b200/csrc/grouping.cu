@@ -220,19 +220,31 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
   uint32_t gcur = G0;
   int nslots = 0, nnew = 0;
   bool ovf = false;
+  // software prefetch of the next term's anti row and candidates
+  uint32_t aw_n = bn > 0 ? G.anti[lane] : 0u;
+  int nf_n = bn > 0 ? G.nfit[0] : 0;
+  int32_t fk_n = (bn > 0 && lane < kGK) ? G.fitk[lane] : -1;
   for (int i = 0; i < bn && !ovf; ++i) {
     // anti-commutation with earlier batch terms only (u < i)
-    uint32_t aw = G.anti[(int64_t)i * kGAW + lane];
+    uint32_t aw = aw_n;
+    const int nf = nf_n;
+    const int32_t fk = fk_n;
+    if (i + 1 < bn) {
+      aw_n = G.anti[(int64_t)(i + 1) * kGAW + lane];
+      nf_n = G.nfit[i + 1];
+      fk_n = lane < kGK ? G.fitk[(i + 1) * kGK + lane] : -1;
+    }
     const int wi = i >> 5;
     aw = lane < wi ? aw : (lane == wi ? (aw & ((1u << (i & 31)) - 1u)) : 0u);
-    const int nf = G.nfit[i];
-    const int32_t fk = lane < kGK ? G.fitk[i * kGK + lane] : -1;
-    int chosen = -1;
+    int chosen = -1, cslot = -2;  // cslot: slot of `chosen` (-1 none yet, -2 unknown)
     const int ncand = nf < kGK ? nf : kGK;
     for (int k = 0; k < ncand && chosen < 0; ++k) {
       const int c = __shfl_sync(0xffffffffu, fk, k);
       const int s = hfind(R, c);
-      if (s < 0 || !__any_sync(0xffffffffu, (aw & R.mask[s][lane]) != 0u)) chosen = c;
+      if (s < 0 || !__any_sync(0xffffffffu, (aw & R.mask[s][lane]) != 0u)) {
+        chosen = c;
+        cslot = s;
+      }
     }
     if (chosen < 0 && nf > kGK) {  // rare: all first-k candidates blocked
       const int64_t nwords = ((int64_t)G0 + 31) / 32;
@@ -273,12 +285,12 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
       R.mask[s][lane] = 0u;
       ++nnew;
     } else {
-      s = hfind(R, chosen);
+      s = cslot != -2 ? cslot : hfind(R, chosen);
       if (s < 0) {
         s = nslots++;
         if (lane == 0) {
           R.slot_group[s] = chosen;
-          R.slot_old[s] = (int32_t)G.gsize[chosen];
+          R.slot_old[s] = -1;  // pre-existing group: size loaded after the loop
           R.slot_cnt[s] = 0;
           hinsert(R, chosen, s);
         }
@@ -289,7 +301,7 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
     if (lane == wi) R.mask[s][lane] |= 1u << (i & 31);
     if (lane == 0) {
       G.group_of[b0 + i] = chosen;
-      G.member[i] = (uint32_t)(R.slot_old[s] + R.slot_cnt[s]);
+      G.member[i] = (uint32_t)R.slot_cnt[s];  // rank among this batch's members
       G.tslot[i] = s;
       R.slot_cnt[s] += 1;
     }
@@ -302,7 +314,8 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
   // grow every touched group: allocate chunks, link, record chunk tables
   for (int s = lane; s < nslots; s += 32) {
     const int g = R.slot_group[s];
-    const int old = R.slot_old[s], nw = old + R.slot_cnt[s];
+    const int old = R.slot_old[s] < 0 ? (int)G.gsize[g] : R.slot_old[s];
+    const int nw = old + R.slot_cnt[s];
     const int have = (old + 63) / 64, need = (nw + 63) / 64;
     const int add = need - have;
     int base = 0;
@@ -345,8 +358,8 @@ __global__ void __launch_bounds__(kGB, 1) k_group_update(GCtx G, int64_t b0, int
   unsigned long long chk = 0;
   if (i < bn) {
     const int s = G.tslot[i];
-    const uint32_t m = G.member[i];
     const int old = G.slot_old[s];
+    const uint32_t m = (uint32_t)old + G.member[i];  // member index inside the group
     const int chunk = G.slot_chunks[(int64_t)s * kSlotChunks + (int)(m / 64) - old / 64];
     const u64 bit = 1ull << (m & 63);
     const uint32_t off = G.off[b0 + i], cnt = G.off[b0 + i + 1] - off;
