@@ -43,7 +43,7 @@ def commutation_bitmatrix(s: PauliSumSoA, *, row0: int = 0, rows: int | None = N
         out = torch.empty((rows, max(nw, 1)), dtype=torch.int32, device=dev)
     ws_bytes = int(_native.load().pl_bitmatrix_workspace_bytes(S.W, rows))
     if method == "lists":  # worst case: every key bit of every row set
-        ws_bytes += rows * (128 * S.W - 64) * 2
+        ws_bytes += rows * (128 * S.W + 4 - 64) * 4
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     with torch.cuda.device(dev):
         _native.call("pl_commutation_bitmatrix", S.W, M, ptr(S.x), ptr(S.z), S.ld, row0, rows,

@@ -54,10 +54,10 @@ static int launch_bitmatrix(int64_t M, const u64* x, const u64* z, int64_t ld, i
     uint32_t* scratch = (uint32_t*)p;
     p += scan_scratch_words(rows) * 4;
     p = (uint8_t*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
-    uint16_t* list = (uint16_t*)p;
-    const int64_t cap = ((int64_t)ws_bytes - (p - (uint8_t*)ws)) / 2;
+    uint32_t* list = (uint32_t*)p;
+    const int64_t cap = ((int64_t)ws_bytes - (p - (uint8_t*)ws)) / 4;
     const unsigned nb = (unsigned)ceil_div(rows, 256);
-    k_row_weight<W><<<nb, 256, 0, st>>>(x, z, ld, row0, rows, off);
+    k_row_weight<W, 1><<<nb, 256, 0, st>>>(x, z, ld, row0, rows, off);
     PLB_CHECK_LAUNCH("k_row_weight");
     int rc = exclusive_scan_u32(off, off, rows, scratch, off + rows, st);
     if (rc) return rc;
@@ -75,7 +75,7 @@ static int launch_bitmatrix(int64_t M, const u64* x, const u64* z, int64_t ld, i
       }
       method = 2;
     } else {
-      k_row_fill<W><<<nb, 256, 0, st>>>(x, z, ld, row0, rows, off, list);
+      k_row_fill<W, 1><<<nb, 256, 0, st>>>(x, z, ld, row0, rows, off, list);
       PLB_CHECK_LAUNCH("k_row_fill");
       const int64_t colblocks = ceil_div(cols, kColsPerCta);
       int64_t splits = ceil_div(2 * num_sms(), colblocks);
@@ -84,13 +84,13 @@ static int launch_bitmatrix(int64_t M, const u64* x, const u64* z, int64_t ld, i
       if (splits < 1) splits = 1;
       if (splits > 65535) splits = 65535;
       const int64_t rps = ceil_div(rows, splits);
-      const size_t smem = (size_t)32 * (128 * W + kTPad) * 4;
-      auto kern = k_bitmatrix_lists<W>;
+      const size_t smem = lists64_smem_bytes<W>();
+      auto kern = k_bitmatrix_lists64<W>;
       PLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       for (int64_t cbase = 0; cbase < colblocks; cbase += 65535) {
         const int64_t nblk = colblocks - cbase < 65535 ? colblocks - cbase : 65535;
         dim3 grid((unsigned)nblk, (unsigned)splits);
-        StageTimer t_(st, "k_bitmatrix_lists");
+        StageTimer t_(st, "k_bitmatrix_lists64");
         kern<<<grid, 1024, smem, st>>>(x, z, ld, M, row0, rows, col0 + cbase * kColsPerCta,
                                        cols - cbase * kColsPerCta, off, list,
                                        bits + cbase * (kColsPerCta / 32), ld_bits, rps);
@@ -122,7 +122,7 @@ using namespace plb;
 extern "C" int64_t pl_bitmatrix_workspace_bytes(int W, int64_t rows) {
   (void)W;
   if (rows < 0) return 0;
-  return (rows + 1) * 4 + scan_scratch_words(rows) * 4 + 16 + list_capacity_entries(rows) * 2;
+  return (rows + 1) * 4 + scan_scratch_words(rows) * 4 + 16 + list_capacity_entries(rows) * 4;
 }
 
 extern "C" int pl_commutation_bitmatrix(int W, int64_t M, const uint64_t* x, const uint64_t* z,

@@ -908,6 +908,8 @@ static Dims to_dims(const pl_merge_plan& P) {
   D.n = P.n_items;
   D.ma = P.ma;
   D.mb = P.mb;
+  D.n_space = P.n_items;
+  D.j0 = 0;
   D.nb1 = P.n_buckets;
   D.nsamp = P.n_samples;
   D.leaf_cap = P.leaf_cap;

@@ -530,7 +530,7 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
                                 (int)fit_smem));
   PLB_CUDA(cudaFuncSetAttribute(k_group_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(ResolveSmem)));
-  const size_t lists_smem = (size_t)32 * (128 * W + kTPad) * 4;
+  const size_t lists_smem = lists_smem_bytes<(W <= 8 ? W : 8)>();
   if (W <= 8) {
     PLB_CUDA(cudaFuncSetAttribute(k_bitmatrix_lists<W>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lists_smem));

@@ -211,3 +211,33 @@ def test_dense_matrix_small(cuda):
             A = pl.PauliSumSoA.from_terms([(complex(*r.normal(size=2)), l) for l in la], device=cuda)
             B = pl.PauliSumSoA.from_terms([(complex(*r.normal(size=2)), l) for l in lb], device=cuda)
             assert np.allclose(dense(A) @ dense(B), dense(A * B), atol=1e-12)
+
+
+def test_buckets_balanced(cuda):
+    """Performance guard: the sampled splitters must spread config-4 items over
+    the level-1 buckets (a degenerate sample sends everything to one bucket,
+    which stays correct but is ~20x slower)."""
+    import ctypes as C
+    import torch
+    from paper_2605_25974_b200 import _native
+    from paper_2605_25974_b200._device import ptr, stream_ptr
+
+    a, b = rng.config_columns(4, scale=0.2)
+    A, B = soa(500, a, cuda).planes(), soa(500, b, cuda).planes()
+    plan = _native.MergePlan()
+    _native.call("pl_outer_plan", 8, A.M, B.M, ptr(A.x), ptr(A.z), A.ld, ptr(B.x), ptr(B.z), B.ld,
+                 C.byref(plan), stream_ptr(cuda))
+    nb = plan.n_buckets
+    assert nb > 16
+    lib = _native.load()
+    send_bytes = A.M * B.M * lib.pl_dist_item_bytes(C.byref(plan))
+    ws = torch.empty(lib.pl_dist_workspace_bytes(C.byref(plan), A.M * B.M, nb), dtype=torch.uint8,
+                     device=cuda)
+    send = torch.empty(send_bytes, dtype=torch.uint8, device=cuda)
+    counts = torch.empty(nb, dtype=torch.int32, device=cuda)
+    _native.call("pl_outer_partition", C.byref(plan), ptr(A.x), ptr(A.z), ptr(A.k), A.ld, ptr(B.x),
+                 ptr(B.z), ptr(B.k), B.ld, 0, B.M, ptr(ws), ws.numel(), ptr(send), ptr(counts),
+                 stream_ptr(cuda))
+    cnt = counts.cpu().numpy()
+    assert cnt.sum() == A.M * B.M
+    assert cnt.max() < 4 * cnt.mean(), (cnt.max(), cnt.mean())
