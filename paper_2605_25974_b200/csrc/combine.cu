@@ -1006,7 +1006,7 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const O
   const size_t lsm = leaf_smem_bytes(KW);
   auto lk = k_leaves<W, KW, MODE>;
   if (set_smem(lk, lsm)) return PL_ERR_CUDA;
-  const int grid = 4 * num_sms();
+  const int grid = kLeafCtasPerSm * num_sms();
   StageTimer t_(st, "k_leaves");
   lk<<<grid, kLeafThreads2, lsm, st>>>(L, D, S, C, O);
   PLB_CHECK_LAUNCH("k_leaves");
@@ -1167,7 +1167,7 @@ static int run_merge_received(const pl_merge_plan& P, const u64* recv, int64_t n
   auto lk = k_leaves<W, KW, 0>;
   if (set_smem(lk, lsm)) return PL_ERR_CUDA;
   StageTimer t_(st, "k_leaves");
-  lk<<<4 * num_sms(), kLeafThreads2, lsm, st>>>(L, D, S, C, O);
+  lk<<<kLeafCtasPerSm * num_sms(), kLeafThreads2, lsm, st>>>(L, D, S, C, O);
   PLB_CHECK_LAUNCH("k_leaves");
   return PL_OK;
 }

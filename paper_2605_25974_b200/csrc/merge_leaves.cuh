@@ -19,7 +19,18 @@
 // processed synchronously, tile by tile.
 #pragma once
 
+// Shared-memory items per leaf buffer for key width KW (two buffers of about
+// 23 KB per CTA so four CTAs fit on one SM).
+__host__ __device__ constexpr int leaf_cap_for(int KW) {
+  return KW <= 2 ? 1024 : KW == 4 ? 512 : KW == 8 ? 256 : KW == 16 ? 128 : 64;
+}
+
+__host__ __device__ constexpr size_t leaf_smem_bytes(int KW) {
+  return 2 * (((size_t)leaf_cap_for(KW) * (8 * KW + 4 + 2 + 1) + 15) & ~(size_t)15) + 64;
+}
+
 constexpr int kLeafThreads2 = 256;
+constexpr int kLeafCtasPerSm = 3;  // 85 registers per thread, no spills in the hot path
 constexpr int kLeafWarps2 = kLeafThreads2 / 32;
 
 template <int KW>
@@ -37,11 +48,102 @@ __device__ __forceinline__ void cmp_swap(u64* K, uint32_t* I, int64_t stride, in
   }
 }
 
-// Bitonic sort of n items in shared memory with warp-local stages.
-template <int KW>
-__device__ void bitonic_sort_local(u64* K, uint32_t* I, int stride, int n) {
+// Straight-line compare-exchange with a compile-time stride: both items are
+// loaded once, compared branch-free and written back only when out of order.
+template <int KW, int STRIDE>
+__device__ __forceinline__ void cex(u64* __restrict__ K, uint32_t* __restrict__ I, int i, int p) {
+  u64 a[KW], b[KW];
+#pragma unroll
+  for (int d = 0; d < KW; ++d) {
+    a[d] = K[d * STRIDE + i];
+    b[d] = K[d * STRIDE + p];
+  }
+  const uint32_t ia = I[i], ib = I[p];
+  // b < a ?  (lexicographic over key words, then ik)
+  bool lt = ib < ia, eq = true;
+#pragma unroll
+  for (int d = KW - 1; d >= 0; --d) {
+    lt = (b[d] < a[d]) || (b[d] == a[d] && lt);
+    (void)eq;
+  }
+  if (lt) {
+#pragma unroll
+    for (int d = 0; d < KW; ++d) {
+      K[d * STRIDE + i] = b[d];
+      K[d * STRIDE + p] = a[d];
+    }
+    I[i] = ib;
+    I[p] = ia;
+  }
+}
+
+// Fully unrolled bitonic network for NPOW (power of two) slots: every stage's
+// partner distance and locality are compile-time constants.
+template <int KW, int STRIDE, int NPOW>
+__device__ __forceinline__ void bitonic_fixed(u64* K, uint32_t* I, int n) {
+  constexpr int HALF = NPOW / 2;
+  constexpr int SEG = NPOW / kLeafWarps2;  // elements owned by one warp
+  constexpr int PER = HALF / kLeafWarps2;  // pairs per warp in local stages
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  bool prev_local = false;  // folded to constants: both loops are fully unrolled
+#pragma unroll
+  for (int k = 2; k <= NPOW; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const bool flip = j == (k >> 1);
+      const int xr = flip ? (k - 1) : j;
+      const bool local = SEG >= 2 && (flip ? k : 2 * j) <= SEG;
+      if (local) {
+        if (PER >= 1) {
+#pragma unroll
+          for (int t0 = 0; t0 < (PER + 31) / 32; ++t0) {
+            const int t = warp * PER + t0 * 32 + lane;
+            if (t0 * 32 + lane < PER) {
+              const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+              const int p = i ^ xr;
+              if (p < n) cex<KW, STRIDE>(K, I, i, p);
+            }
+          }
+        }
+        __syncwarp();
+      } else {
+        if (prev_local) __syncthreads();
+#pragma unroll
+        for (int t0 = 0; t0 < (HALF + kLeafThreads2 - 1) / kLeafThreads2; ++t0) {
+          const int t = t0 * kLeafThreads2 + threadIdx.x;
+          if (t < HALF) {
+            const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+            const int p = i ^ xr;
+            if (p < n) cex<KW, STRIDE>(K, I, i, p);
+          }
+        }
+        __syncthreads();
+      }
+      prev_local = local;
+    }
+  }
+  __syncthreads();
+}
+
+// Bitonic sort of n items in shared memory with warp-local stages
+// (STRIDE = leaf capacity, a compile-time constant).
+template <int KW, int STRIDE>
+__device__ void bitonic_sort_local(u64* K, uint32_t* I, int n) {
   int npow = 1;
   while (npow < n) npow <<= 1;
+  switch (npow) {
+    case 2: bitonic_fixed<KW, STRIDE, 2>(K, I, n); return;
+    case 4: bitonic_fixed<KW, STRIDE, 4>(K, I, n); return;
+    case 8: bitonic_fixed<KW, STRIDE, 8>(K, I, n); return;
+    case 16: bitonic_fixed<KW, STRIDE, 16>(K, I, n); return;
+    case 32: bitonic_fixed<KW, STRIDE, 32>(K, I, n); return;
+    case 64: bitonic_fixed<KW, STRIDE, 64>(K, I, n); return;
+    case 128: bitonic_fixed<KW, STRIDE, 128>(K, I, n); return;
+    case 256: if (STRIDE >= 256) { bitonic_fixed<KW, STRIDE, (STRIDE >= 256 ? 256 : 2)>(K, I, n); return; } break;
+    case 512: if (STRIDE >= 512) { bitonic_fixed<KW, STRIDE, (STRIDE >= 512 ? 512 : 2)>(K, I, n); return; } break;
+    case 1024: if (STRIDE >= 1024) { bitonic_fixed<KW, STRIDE, (STRIDE >= 1024 ? 1024 : 2)>(K, I, n); return; } break;
+    default: break;
+  }
   const int half = npow >> 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int seg = npow / kLeafWarps2;  // elements owned by one warp
@@ -52,19 +154,20 @@ __device__ void bitonic_sort_local(u64* K, uint32_t* I, int stride, int n) {
       const bool flip = j == (k >> 1);
       const int blk = flip ? k : 2 * j;
       const bool local = seg >= 2 && blk <= seg;
+      const int xr = flip ? (k - 1) : j;
       if (local) {
         for (int t = warp * per + lane; t < (warp + 1) * per; t += 32) {
           const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
-          const int p = flip ? (i ^ (k - 1)) : (i + j);
-          if (p < n) cmp_swap<KW>(K, I, stride, i, p);
+          const int p = i ^ xr;
+          if (p < n) cex<KW, STRIDE>(K, I, i, p);
         }
         __syncwarp();
       } else {
         if (prev_local) __syncthreads();
         for (int t = threadIdx.x; t < half; t += kLeafThreads2) {
           const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
-          const int p = flip ? (i ^ (k - 1)) : (i + j);
-          if (p < n) cmp_swap<KW>(K, I, stride, i, p);
+          const int p = i ^ xr;
+          if (p < n) cex<KW, STRIDE>(K, I, i, p);
         }
         __syncthreads();
       }
@@ -171,10 +274,10 @@ __device__ __forceinline__ LeafBuf<KW> leaf_buf(u64* sm, int cap, int b) {
 }
 
 template <int W, int KW, int MODE>
-__global__ void __launch_bounds__(kLeafThreads2, 4)
+__global__ void __launch_bounds__(kLeafThreads2, kLeafCtasPerSm)
 k_leaves(Layout L, Dims D, SrcA S, Ctl C, OutP O) {
   extern __shared__ u64 sm[];
-  const int cap = D.leaf_cap;
+  constexpr int cap = leaf_cap_for(KW);  // == D.leaf_cap
   __shared__ uint32_t s_leaf;
   __shared__ uint32_t s_warp[kLeafWarps2];
   __shared__ uint64_t s_base;
@@ -289,7 +392,7 @@ k_leaves(Layout L, Dims D, SrcA S, Ctl C, OutP O) {
         B.I[t] = GI[t];
       }
       __syncthreads();
-      if (n > 1) bitonic_sort_local<KW>(B.K, B.I, cap, n);
+      if (n > 1) bitonic_sort_local<KW, cap>(B.K, B.I, n);
       for (int p = tid; p < n; p += kLeafThreads2)
         B.HEAD[p] = (p == 0 || !key_eq<KW>(B.K, cap, p, p - 1)) ? 1 : 0;
       __syncthreads();
@@ -322,12 +425,3 @@ k_leaves(Layout L, Dims D, SrcA S, Ctl C, OutP O) {
   }
 }
 
-// Shared-memory items per leaf buffer for key width KW (two buffers of about
-// 23 KB per CTA so four CTAs fit on one SM).
-__host__ __device__ constexpr int leaf_cap_for(int KW) {
-  return KW <= 2 ? 1024 : KW == 4 ? 512 : KW == 8 ? 256 : KW == 16 ? 128 : 64;
-}
-
-__host__ __device__ constexpr size_t leaf_smem_bytes(int KW) {
-  return 2 * (((size_t)leaf_cap_for(KW) * (8 * KW + 4 + 2 + 1) + 15) & ~(size_t)15) + 64;
-}
