@@ -61,7 +61,7 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
         for o in BUILD.glob("*.o"):
             o.unlink()
     hm = _headers_mtime()
-    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+    with ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(lambda s: _compile(s, hm, verbose), srcs))
     newest = max(o.stat().st_mtime for o in objs)
     if force or not LIB.exists() or LIB.stat().st_mtime < newest:

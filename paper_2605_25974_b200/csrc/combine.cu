@@ -1,1231 +1,13 @@
-// K2-K4: outer product + simplify, and sort_and_combine.
-//
-// Restates _combine_columns (sums.py:94-120) applied to the raw outer product
-// of _multiply_columns (sums.py:144-174), without ever materialising the raw
-// 145-byte records:
-//
-//   item      = (packed key, ik)  where ik = raw_row << 2 | k,
-//               raw_row = j*Ma + i (the reference's j-major row, sums.py:137)
-//   key       = the canonical (z0..z{W-1}, x0..x{W-1}) big-endian string
-//               (sums.py:104-106, strings.py:165-167) with every bit range that
-//               is zero in all operands removed; removal of constant bits keeps
-//               the lexicographic order, so sorting packed keys sorts terms.
-//
-// Pipeline (sample sort, every stage a pure function of its input):
-//   1. k_sample   : S deterministic sample keys, bitonic-sorted in one CTA,
-//                   -> nb1-1 splitters (ranges of the key space)
-//   2. k_count    : key of every item -> bucket (binary search) -> counts
-//   3. k_buckets  : scan counts -> bucket bases, leaves per bucket
-//   4. k_scatter  : items -> bucket-contiguous buffer 1 (per-CTA reservation)
-//   5. k_split    : buckets larger than a shared-memory leaf are re-partitioned
-//                   by a CTA-local sample into sub-buckets (buffer 2)
-//   6. k_leaves   : per leaf (<= leaf_cap items in shared memory, otherwise
-//                   in place in global memory): bitonic sort by (key, ik),
-//                   detect runs of equal keys, sum each run's coefficients
-//                   a_c[i]*b_c[j]*i^k in raw-row order with numpy's reduceat
-//                   summation tree (one thread per run, bit-exact),
-//                   drop |sum| <= eps, and write the merged terms at the
-//                   position found by a decoupled look-back over leaves.
-// Runs never straddle buckets (splitters compare keys only) and each run is
-// summed by one thread in ik order, so the output is bit-identical whatever
-// the bucket structure, CTA schedule or GPU count.
-#include <algorithm>
-#include <vector>
-
-#include "common.cuh"
+// K2-K4 C ABI: plans, workspace checks and the W dispatch into the per-W
+// instantiations (combine_w*.cu); kernels are in combine_impl.cuh.
+#include "combine_impl.cuh"
 
 namespace plb {
-
-constexpr int kGenThreads = 256;
-constexpr int kGenTB = 16;        // b-terms per tile (outer) / terms per thread (sort)
-constexpr int kLeafThreads = 512;
-constexpr int kSplitThreads = 512;
-constexpr int kSortSmemBytes = 200 * 1024;
-constexpr int kSampleOversample = 16;
-constexpr int kMaxBuckets = 2048;
-
-// ---------------------------------------------------------------- layout
-struct Layout {
-  int W, KW, active;  // active: bit w set if z-word w or x-word w is used
-  int lo[PL_PLAN_MAX_SEG], len[PL_PLAN_MAX_SEG], pos[PL_PLAN_MAX_SEG];
-};
-
-struct Ctl {  // control arrays inside the workspace
-  u64* split;            // [KW][nb1]
-  uint32_t* bcount;      // nb1
-  uint32_t* bbase;       // nb1 + 1
-  uint32_t* bcursor;     // nb1
-  uint32_t* leaf_off;    // nb1 + 1
-  uint32_t* n_leaves;    // 1
-  uint32_t* leaf_ctr;    // 1
-  uint4* leaf_desc;      // max_leaves: (buffer 1|2, offset, size, 0)
-  unsigned long long* leaf_status;  // max_leaves
-  u64* k1;               // [KW][n] item keys, buffer 1
-  uint32_t* i1;          // [n]
-  u64* k2;               // buffer 2
-  uint32_t* i2;
-};
-
-struct Dims {
-  int64_t n, ma, mb;     // items held here; |A|; B columns generated here
-  int64_t n_space, j0;   // full raw-product size (sampling space); first B column
-  int nb1, nsamp, leaf_cap, leaf_target, max_sub, max_leaves;
-};
-
-struct SrcA {  // operands (outer: A and B; sort: A only)
-  const u64 *ax, *az;
-  const uint8_t* ak;
-  const double2* ac;
-  int64_t lda;
-  const u64 *bx, *bz;
-  const uint8_t* bk;
-  const double2* bc;
-  int64_t ldb;
-};
-
-struct OutP {
-  u64 *ox, *oz;
-  uint8_t* ok;
-  double2* oc;
-  int64_t ldo;
-  int64_t* count;
-  double eps;
-};
-
-__host__ __device__ inline int key_words_for_bits(int bits) {
-  const int kw = (bits + 63) / 64;
-  int p = 1;
-  while (p < kw) p <<= 1;
-  return p;
-}
-
-__host__ __device__ inline u64 low_mask(int len) { return len >= 64 ? ~0ull : ((1ull << len) - 1); }
-
-template <int KW>
-__device__ __forceinline__ void put_seg(u64 (&key)[KW], u64 v, int pos, int len) {
-  const int wi = pos >> 6, off = pos & 63;
-  const int shift = 64 - off - len;
-  const u64 a = shift >= 0 ? (v << shift) : (v >> (-shift));
-  const u64 b = shift >= 0 ? 0ull : (v << (64 + shift));
-#pragma unroll
-  for (int d = 0; d < KW; ++d) {
-    if (d == wi) key[d] |= a;
-    if (d == wi + 1) key[d] |= b;
-  }
-}
-
-template <int KW>
-__device__ __forceinline__ u64 get_seg(const u64 (&key)[KW], int pos, int len) {
-  const int wi = pos >> 6, off = pos & 63;
-  u64 a = 0, b = 0;
-#pragma unroll
-  for (int d = 0; d < KW; ++d) {
-    if (d == wi) a = key[d];
-    if (d == wi + 1) b = key[d];
-  }
-  const u64 hi = off ? ((a << off) | (b >> (64 - off))) : a;
-  return hi >> (64 - len);
-}
-
-// canonical words (z[W], x[W]) -> packed key
-template <int W, int KW>
-__device__ __forceinline__ void pack_key(const Layout& L, const u64 (&zc)[W], const u64 (&xc)[W],
-                                         u64 (&key)[KW]) {
-#pragma unroll
-  for (int d = 0; d < KW; ++d) key[d] = 0;
-#pragma unroll
-  for (int s = 0; s < 2 * W; ++s) {
-    const int len = L.len[s];
-    if (len) {
-      const u64 w = s < W ? zc[s] : xc[s - W];
-      put_seg<KW>(key, (w >> L.lo[s]) & low_mask(len), L.pos[s], len);
-    }
-  }
-}
-
-template <int KW>
-__device__ __forceinline__ void load_key(const u64* k, int64_t stride, int64_t i, u64 (&key)[KW]) {
-#pragma unroll
-  for (int d = 0; d < KW; ++d) key[d] = k[d * stride + i];
-}
-
-template <int KW>
-__device__ __forceinline__ void store_key(u64* k, int64_t stride, int64_t i, const u64 (&key)[KW]) {
-#pragma unroll
-  for (int d = 0; d < KW; ++d) k[d * stride + i] = key[d];
-}
-
-// key <= splitter[b] ?  (lexicographic)
-template <int KW>
-__device__ __forceinline__ bool key_lt(const u64 (&a)[KW], const u64* s, int64_t stride, int b) {
-#pragma unroll
-  for (int d = 0; d < KW; ++d) {
-    const u64 v = s[d * stride + b];
-    if (a[d] != v) return a[d] < v;
-  }
-  return false;
-}
-
-// number of splitters <= key  (upper bound); splitters s[0..nsp)
-template <int KW>
-__device__ __forceinline__ int bucket_of(const u64 (&key)[KW], const u64* s, int64_t stride,
-                                         int nsp) {
-  int lo = 0, hi = nsp;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (key_lt<KW>(key, s, stride, mid)) hi = mid;
-    else lo = mid + 1;
-  }
-  return lo;
-}
-
-// item order: (key, ik)
-template <int KW>
-__device__ __forceinline__ bool item_lt(const u64* K, const uint32_t* I, int64_t stride, int a,
-                                        int b) {
-#pragma unroll
-  for (int d = 0; d < KW; ++d) {
-    const u64 ka = K[d * stride + a], kb = K[d * stride + b];
-    if (ka != kb) return ka < kb;
-  }
-  return I[a] < I[b];
-}
-
-template <int KW>
-__device__ __forceinline__ bool key_eq(const u64* K, int64_t stride, int a, int b) {
-#pragma unroll
-  for (int d = 0; d < KW; ++d)
-    if (K[d * stride + a] != K[d * stride + b]) return false;
-  return true;
-}
-
-// Block-wide bitonic sort (all comparators ascending; elements at index >= n
-// behave as +inf so no padding is stored).  Works on shared or global memory.
-template <int KW>
-__device__ void bitonic_sort(u64* K, uint32_t* I, int64_t stride, int n) {
-  int npow = 1;
-  while (npow < n) npow <<= 1;
-  for (int k = 2; k <= npow; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = threadIdx.x; t < (npow >> 1); t += blockDim.x) {
-        const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
-        const int p = (j == (k >> 1)) ? (i ^ (k - 1)) : (i + j);
-        if (p < n && item_lt<KW>(K, I, stride, p, i)) {
-#pragma unroll
-          for (int d = 0; d < KW; ++d) {
-            const u64 tmp = K[d * stride + i];
-            K[d * stride + i] = K[d * stride + p];
-            K[d * stride + p] = tmp;
-          }
-          const uint32_t ti = I[i];
-          I[i] = I[p];
-          I[p] = ti;
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
-// Complex product rounded exactly like numpy's complex128 multiply on
-// FMA-capable x86 hosts (the reference's sums.py:141):
-//   re = fma(ar, br, -(ai*bi)),  im = fma(ar, bi, ai*br)
-// (verified bit-for-bit against numpy 2.3.5).
-__device__ __forceinline__ double2 cmul_np(double2 a, double2 b) {
-  return make_double2(__fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y)),
-                      __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x)));
-}
-
-// c * i^k  (exact)
-__device__ __forceinline__ double2 rot_ik(double2 c, int k) {
-  switch (k & 3) {
-    case 0: return c;
-    case 1: return make_double2(-c.y, c.x);
-    case 2: return make_double2(-c.x, -c.y);
-    default: return make_double2(c.y, -c.x);
-  }
-}
-
-// ------------------------------------------------------------ item sources
-// MODE 0: outer product A*B; MODE 1: one sum (sort_and_combine).
-template <int W, int KW, int MODE>
-struct Source {
-  // key + phase of raw item r (used by the sampler; slow path, global loads)
-  static __device__ __forceinline__ void item_at(const Layout& L, const SrcA& S, int64_t ma,
-                                                 int64_t r, u64 (&key)[KW], int& k) {
-    u64 zc[W], xc[W];
-    if (MODE == 0) {
-      const int64_t j = (uint32_t)r / (uint32_t)ma, i = r - j * ma;
-      k = (S.ak ? S.ak[i] : 0) + (S.bk ? S.bk[j] : 0);
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        if (L.active >> w & 1) {
-          const u64 a_x = S.ax[w * S.lda + i], a_z = S.az[w * S.lda + i];
-          const u64 b_x = S.bx[w * S.ldb + j], b_z = S.bz[w * S.ldb + j];
-          k += phase_word(a_x, a_z, b_x, b_z);
-          xc[w] = a_x ^ b_x;
-          zc[w] = a_z ^ b_z;
-        } else {
-          xc[w] = zc[w] = 0;
-        }
-      }
-    } else {
-      k = S.ak ? S.ak[r] : 0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        const bool on = L.active >> w & 1;
-        xc[w] = on ? S.ax[w * S.lda + r] : 0ull;
-        zc[w] = on ? S.az[w * S.lda + r] : 0ull;
-      }
-    }
-    pack_key<W, KW>(L, zc, xc, key);
-  }
-
-  static __device__ __forceinline__ double2 coef(const SrcA& S, int64_t ma, uint32_t ik) {
-    const int64_t r = ik >> 2;
-    if (MODE == 0) {
-      const int64_t j = (uint32_t)r / (uint32_t)ma, i = r - j * ma;
-      return rot_ik(cmul_np(S.ac[i], S.bc[j]), (int)(ik & 3));
-    } else {
-      return rot_ik(S.ac[r], (int)(ik & 3));
-    }
-  }
-};
-
-// Sum of one run of equal keys in raw-row order, reproducing numpy's
-// np.add.reduceat (sums.py:112) bit for bit: out = c0 + pairwise(c1..c{m-1}),
-// where numpy's pairwise sum (complex128, PW_BLOCKSIZE 128 doubles) adds
-// fewer than 4 elements left to right from -0.0, blocks of <= 64 elements
-// with 4 interleaved accumulators ((r0+r1)+(r2+r3)) plus a sequential tail,
-// and splits longer ranges at a multiple of 4 elements near the middle.
-// Verified against numpy 2.3.5.
-template <int W, int KW, int MODE>
-struct RunSum {
-  static __device__ __forceinline__ double2 c(const SrcA& S, int64_t ma, const uint32_t* I,
-                                              int64_t e) {
-    return Source<W, KW, MODE>::coef(S, ma, I[e]);
-  }
-  static __device__ double2 block(const SrcA& S, int64_t ma, const uint32_t* I, int64_t b,
-                                  int64_t L) {
-    if (L < 4) {
-      double rr = -0.0, ri = -0.0;
-      for (int64_t e = 0; e < L; ++e) {
-        const double2 v = c(S, ma, I, b + e);
-        rr = __dadd_rn(rr, v.x);
-        ri = __dadd_rn(ri, v.y);
-      }
-      return make_double2(rr, ri);
-    }
-    double2 r0 = c(S, ma, I, b), r1 = c(S, ma, I, b + 1), r2 = c(S, ma, I, b + 2),
-            r3 = c(S, ma, I, b + 3);
-    int64_t i = 4;
-    const int64_t lim = L - (L % 4);
-    for (; i < lim; i += 4) {
-      const double2 v0 = c(S, ma, I, b + i), v1 = c(S, ma, I, b + i + 1);
-      const double2 v2 = c(S, ma, I, b + i + 2), v3 = c(S, ma, I, b + i + 3);
-      r0.x = __dadd_rn(r0.x, v0.x); r0.y = __dadd_rn(r0.y, v0.y);
-      r1.x = __dadd_rn(r1.x, v1.x); r1.y = __dadd_rn(r1.y, v1.y);
-      r2.x = __dadd_rn(r2.x, v2.x); r2.y = __dadd_rn(r2.y, v2.y);
-      r3.x = __dadd_rn(r3.x, v3.x); r3.y = __dadd_rn(r3.y, v3.y);
-    }
-    double rr = __dadd_rn(__dadd_rn(r0.x, r1.x), __dadd_rn(r2.x, r3.x));
-    double ri = __dadd_rn(__dadd_rn(r0.y, r1.y), __dadd_rn(r2.y, r3.y));
-    for (; i < L; ++i) {
-      const double2 v = c(S, ma, I, b + i);
-      rr = __dadd_rn(rr, v.x);
-      ri = __dadd_rn(ri, v.y);
-    }
-    return make_double2(rr, ri);
-  }
-  // numpy's recursive split, evaluated with an explicit stack (depth <= 25
-  // for runs < 2^30; device recursion would overflow the default stack)
-  static __device__ __noinline__ double2 pairwise(const SrcA& S, int64_t ma, const uint32_t* I,
-                                                  int64_t b, int64_t L) {
-    int64_t sb[32], sl[32];
-    double2 left[32];
-    int sp = 0;
-    sb[0] = b;
-    sl[0] = L;
-    for (;;) {
-      while (sl[sp] > 64) {  // descend into left halves
-        sb[sp + 1] = sb[sp];
-        sl[sp + 1] = (sl[sp] - (sl[sp] % 8)) / 2;
-        left[sp].x = __longlong_as_double(-1);  // marker: left half pending
-        ++sp;
-      }
-      double2 r = block(S, ma, I, sb[sp], sl[sp]);
-      for (;;) {  // ascend
-        if (sp == 0) return r;
-        --sp;
-        if (__double_as_longlong(left[sp].x) == -1LL) {  // r is the left half: go right
-          left[sp] = r;
-          const int64_t e1 = (sl[sp] - (sl[sp] % 8)) / 2;
-          sb[sp + 1] = sb[sp] + e1;
-          sl[sp + 1] = sl[sp] - e1;
-          ++sp;
-          break;
-        }
-        r = make_double2(__dadd_rn(left[sp].x, r.x), __dadd_rn(left[sp].y, r.y));
-      }
-    }
-  }
-  static __device__ __forceinline__ double2 run(const SrcA& S, int64_t ma, const uint32_t* I,
-                                                int64_t p, int64_t m) {
-    const double2 c0 = c(S, ma, I, p);
-    if (m == 1) return c0;
-    const double2 r = m - 1 <= 64 ? block(S, ma, I, p + 1, m - 1) : pairwise(S, ma, I, p + 1, m - 1);
-    return make_double2(__dadd_rn(c0.x, r.x), __dadd_rn(c0.y, r.y));
-  }
-};
-
-// ------------------------------------------------------------- 1. sampler
-template <int W, int KW, int MODE>
-__global__ void __launch_bounds__(kLeafThreads)
-k_sample(Layout L, Dims D, SrcA S, Ctl C) {
-  extern __shared__ u64 sm[];
-  const int ns = D.nsamp;
-  u64* K = sm;
-  uint32_t* I = reinterpret_cast<uint32_t*>(K + (int64_t)KW * ns);
-  for (int s = threadIdx.x; s < ns; s += blockDim.x) {
-    const int64_t r = ((2 * (int64_t)s + 1) * D.n_space) / (2 * (int64_t)ns);
-    u64 key[KW];
-    int k;
-    Source<W, KW, MODE>::item_at(L, S, D.ma, r, key, k);
-    store_key<KW>(K, ns, s, key);
-    I[s] = (uint32_t)s;
-  }
-  __syncthreads();
-  bitonic_sort<KW>(K, I, ns, ns);
-  for (int b = 1 + threadIdx.x; b < D.nb1; b += blockDim.x) {
-    const int src = (int)(((int64_t)b * ns) / D.nb1);
-#pragma unroll
-    for (int d = 0; d < KW; ++d) C.split[d * D.nb1 + (b - 1)] = K[d * ns + src];
-  }
-}
-
-// ---------------------------------------------------- 2./4. count, scatter
-// Shared memory: splitters [KW][nb1] | hist nb1 | gbase nb1 | tile | (b, r) per item
-struct GenSmem {
-  u64* split;
-  uint32_t* hist;
-  uint32_t* gbase;
-  u64* tile;  // outer: [2W][kGenTB] b-term words (z then x)
-  uint32_t* slot;  // per item: bucket << 16 | rank  (scatter only)
-};
-
-template <int W>
-__device__ __forceinline__ GenSmem gen_smem(u64* sm, int nb1, int KW) {
-  GenSmem g;
-  g.split = sm;
-  g.hist = reinterpret_cast<uint32_t*>(sm + (int64_t)KW * nb1);
-  g.gbase = g.hist + nb1;
-  g.tile = reinterpret_cast<u64*>(g.gbase + nb1);  // 2*nb1 u32 keeps 8-byte alignment
-  g.slot = reinterpret_cast<uint32_t*>(g.tile + 2 * W * kGenTB);
-  return g;
-}
-
-template <int KW>
-__device__ __forceinline__ void gen_prologue(const GenSmem& g, const Ctl& C, int nb1) {
-  for (int b = threadIdx.x; b < nb1; b += blockDim.x) {
-    g.hist[b] = 0;
-    if (b < nb1 - 1) {
-#pragma unroll
-      for (int d = 0; d < KW; ++d) g.split[d * nb1 + b] = C.split[d * nb1 + b];
-    }
-  }
-}
-
-// Per-thread item generator.  Outer: thread = a-term i, items (i, j0+jj).
-// Sort: thread handles terms base + jj*blockDim + tid.
-template <int W, int KW, int MODE>
-struct Gen {
-  u64 ax[W], az[W];
-  int ka;
-  int64_t i;
-  bool valid_i;
-
-  __device__ __forceinline__ void init(const Layout& L, const Dims& D, const SrcA& S,
-                                       const GenSmem& g) {
-    if (MODE == 0) {
-      i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-      valid_i = i < D.ma;
-      const int64_t j0 = D.j0 + (int64_t)blockIdx.y * kGenTB;
-      // b tile into shared memory (z words then x words)
-      for (int t = threadIdx.x; t < 2 * W * kGenTB; t += blockDim.x) {
-        const int s = t / kGenTB, jj = t % kGenTB;
-        const int w = s < W ? s : s - W;
-        const int64_t j = j0 + jj;
-        u64 v = 0;
-        if (j < D.j0 + D.mb && (L.active >> w & 1))
-          v = s < W ? S.bz[w * S.ldb + j] : S.bx[w * S.ldb + j];
-        g.tile[s * kGenTB + jj] = v;
-      }
-      ka = 0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        const bool on = valid_i && (L.active >> w & 1);
-        ax[w] = on ? S.ax[w * S.lda + i] : 0ull;
-        az[w] = on ? S.az[w * S.lda + i] : 0ull;
-      }
-      if (valid_i && S.ak) ka = S.ak[i];
-    }
-  }
-
-  // item jj of this thread: returns false when out of range
-  __device__ __forceinline__ bool item(const Layout& L, const Dims& D, const SrcA& S,
-                                       const GenSmem& g, int jj, u64 (&key)[KW], uint32_t& ik) {
-    u64 zc[W], xc[W];
-    int64_t r;
-    int k;
-    if (MODE == 0) {
-      const int64_t j = D.j0 + (int64_t)blockIdx.y * kGenTB + jj;  // global B index
-      if (!valid_i || j >= D.j0 + D.mb) return false;
-      k = ka + (S.bk ? S.bk[j] : 0);
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        if (L.active >> w & 1) {
-          const u64 b_z = g.tile[w * kGenTB + jj], b_x = g.tile[(W + w) * kGenTB + jj];
-          k += phase_word(ax[w], az[w], b_x, b_z);
-          xc[w] = ax[w] ^ b_x;
-          zc[w] = az[w] ^ b_z;
-        } else {
-          xc[w] = zc[w] = 0;
-        }
-      }
-      r = j * D.ma + i;
-    } else {
-      r = (int64_t)blockIdx.x * blockDim.x * kGenTB + (int64_t)jj * blockDim.x + threadIdx.x;
-      if (r >= D.n) return false;
-      k = S.ak ? S.ak[r] : 0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        const bool on = L.active >> w & 1;
-        xc[w] = on ? S.ax[w * S.lda + r] : 0ull;
-        zc[w] = on ? S.az[w * S.lda + r] : 0ull;
-      }
-    }
-    pack_key<W, KW>(L, zc, xc, key);
-    ik = ((uint32_t)r << 2) | (uint32_t)(k & 3);
-    return true;
-  }
-};
-
-template <int W, int KW, int MODE>
-__global__ void __launch_bounds__(kGenThreads)
-k_count(Layout L, Dims D, SrcA S, Ctl C) {
-  extern __shared__ u64 sm[];
-  const GenSmem g = gen_smem<W>(sm, D.nb1, KW);
-  gen_prologue<KW>(g, C, D.nb1);
-  Gen<W, KW, MODE> gen;
-  gen.init(L, D, S, g);
-  __syncthreads();
-#pragma unroll 1
-  for (int jj = 0; jj < kGenTB; ++jj) {
-    u64 key[KW];
-    uint32_t ik;
-    if (gen.item(L, D, S, g, jj, key, ik)) {
-      const int b = bucket_of<KW>(key, g.split, D.nb1, D.nb1 - 1);
-      atomicAdd(&g.hist[b], 1u);
-    }
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < D.nb1; b += blockDim.x)
-    if (g.hist[b]) atomicAdd(&C.bcount[b], g.hist[b]);
-}
-
-template <int W, int KW, int MODE>
-__global__ void __launch_bounds__(kGenThreads)
-k_scatter(Layout L, Dims D, SrcA S, Ctl C) {
-  extern __shared__ u64 sm[];
-  const GenSmem g = gen_smem<W>(sm, D.nb1, KW);
-  gen_prologue<KW>(g, C, D.nb1);
-  Gen<W, KW, MODE> gen;
-  gen.init(L, D, S, g);
-  __syncthreads();
-#pragma unroll 1
-  for (int jj = 0; jj < kGenTB; ++jj) {
-    u64 key[KW];
-    uint32_t ik;
-    uint32_t code = 0xFFFFFFFFu;
-    if (gen.item(L, D, S, g, jj, key, ik)) {
-      const int b = bucket_of<KW>(key, g.split, D.nb1, D.nb1 - 1);
-      const uint32_t rk = atomicAdd(&g.hist[b], 1u);
-      code = ((uint32_t)b << 16) | rk;
-    }
-    g.slot[jj * kGenThreads + threadIdx.x] = code;
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < D.nb1; b += blockDim.x)
-    if (g.hist[b]) g.gbase[b] = atomicAdd(&C.bcursor[b], g.hist[b]);
-  __syncthreads();
-#pragma unroll 1
-  for (int jj = 0; jj < kGenTB; ++jj) {
-    const uint32_t code = g.slot[jj * kGenThreads + threadIdx.x];
-    if (code == 0xFFFFFFFFu) continue;
-    u64 key[KW];
-    uint32_t ik;
-    gen.item(L, D, S, g, jj, key, ik);
-    const uint32_t pos = g.gbase[code >> 16] + (code & 0xFFFFu);
-    store_key<KW>(C.k1, D.n, pos, key);
-    C.i1[pos] = ik;
-  }
-}
-
-// ------------------------------------------------------------ 3. buckets
-__device__ __forceinline__ int leaves_for(uint32_t size, const Dims& D) {
-  if (size == 0) return 0;
-  if ((int)size <= D.leaf_cap) return 1;
-  int64_t s = ((int64_t)size + D.leaf_target - 1) / D.leaf_target;
-  return (int)(s < D.max_sub ? s : D.max_sub);
-}
-
-__global__ void __launch_bounds__(1024) k_buckets(Dims D, Ctl C, int64_t* out_count) {
-  __shared__ uint32_t wsum[32], wsum2[32];
-  __shared__ uint32_t carry, carry2;
-  if (threadIdx.x == 0) {
-    carry = 0;
-    carry2 = 0;
-    if (D.nb1 == 1) C.bcount[0] = (uint32_t)D.n;
-    *C.leaf_ctr = 0;
-    *out_count = 0;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int base = 0; base < D.nb1; base += blockDim.x) {
-    const int b = base + threadIdx.x;
-    const uint32_t v = b < D.nb1 ? C.bcount[b] : 0;
-    const uint32_t nl = b < D.nb1 ? (uint32_t)leaves_for(v, D) : 0;
-    uint32_t a = v, c = nl;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t ta = __shfl_up_sync(0xffffffffu, a, o);
-      const uint32_t tc = __shfl_up_sync(0xffffffffu, c, o);
-      if (lane >= o) { a += ta; c += tc; }
-    }
-    if (lane == 31) { wsum[wid] = a; wsum2[wid] = c; }
-    __syncthreads();
-    if (wid == 0) {
-      uint32_t s = wsum[lane], s2 = wsum2[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, s, o);
-        const uint32_t t2 = __shfl_up_sync(0xffffffffu, s2, o);
-        if (lane >= o) { s += t; s2 += t2; }
-      }
-      wsum[lane] = s;
-      wsum2[lane] = s2;
-    }
-    __syncthreads();
-    const uint32_t ex = carry + (wid ? wsum[wid - 1] : 0) + a - v;
-    const uint32_t ex2 = carry2 + (wid ? wsum2[wid - 1] : 0) + c - nl;
-    if (b < D.nb1) {
-      C.bbase[b] = ex;
-      C.bcursor[b] = ex;
-      C.leaf_off[b] = ex2;
-    }
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) {
-      carry = ex + v;
-      carry2 = ex2 + nl;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    C.bbase[D.nb1] = carry;
-    C.leaf_off[D.nb1] = carry2;
-    *C.n_leaves = carry2;
-  }
-}
-
-// -------------------------------------------------------------- 5. split
-template <int KW>
-__global__ void __launch_bounds__(kSplitThreads)
-k_split(Dims D, Ctl C, int s2cap) {
-  extern __shared__ u64 sm[];
-  const int b = blockIdx.x;
-  const uint32_t size = C.bcount[b], base = C.bbase[b];
-  const uint32_t lo = C.leaf_off[b];
-  if (size == 0) return;
-  if ((int)size <= D.leaf_cap) {
-    if (threadIdx.x == 0) C.leaf_desc[lo] = make_uint4(1u, base, size, 0u);
-    return;
-  }
-  const int nsub = leaves_for(size, D);
-  int ns = nsub * kSampleOversample;
-  if (ns > s2cap) ns = s2cap;
-  if ((uint32_t)ns > size) ns = (int)size;
-  // smem: sample keys [KW][ns] | sample idx [ns] | split [KW][nsub] | hist, cur [nsub]
-  u64* SK = sm;
-  uint32_t* SI = reinterpret_cast<uint32_t*>(SK + (int64_t)KW * ns);
-  u64* SP = reinterpret_cast<u64*>(SI + ns + (ns & 1));
-  uint32_t* hist = reinterpret_cast<uint32_t*>(SP + (int64_t)KW * nsub);
-  uint32_t* cur = hist + nsub;
-  const u64* K1 = C.k1 + base;
-  const uint32_t* I1 = C.i1 + base;
-  for (int s = threadIdx.x; s < ns; s += blockDim.x) {
-    const int64_t r = ((2 * (int64_t)s + 1) * size) / (2 * (int64_t)ns);
-#pragma unroll
-    for (int d = 0; d < KW; ++d) SK[d * ns + s] = K1[d * D.n + r];
-    SI[s] = (uint32_t)s;
-  }
-  for (int q = threadIdx.x; q < nsub; q += blockDim.x) hist[q] = 0;
-  __syncthreads();
-  bitonic_sort<KW>(SK, SI, ns, ns);
-  for (int q = 1 + threadIdx.x; q < nsub; q += blockDim.x) {
-    const int src = (int)(((int64_t)q * ns) / nsub);
-#pragma unroll
-    for (int d = 0; d < KW; ++d) SP[d * nsub + (q - 1)] = SK[d * ns + src];
-  }
-  __syncthreads();
-  for (uint32_t t = threadIdx.x; t < size; t += blockDim.x) {
-    u64 key[KW];
-    load_key<KW>(K1, D.n, t, key);
-    atomicAdd(&hist[bucket_of<KW>(key, SP, nsub, nsub - 1)], 1u);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t acc = 0;
-    for (int q = 0; q < nsub; ++q) {
-      const uint32_t h = hist[q];
-      cur[q] = acc;
-      C.leaf_desc[lo + q] = make_uint4(2u, base + acc, h, 0u);
-      acc += h;
-    }
-  }
-  __syncthreads();
-  u64* K2 = C.k2 + base;
-  uint32_t* I2 = C.i2 + base;
-  for (uint32_t t = threadIdx.x; t < size; t += blockDim.x) {
-    u64 key[KW];
-    load_key<KW>(K1, D.n, t, key);
-    const int q = bucket_of<KW>(key, SP, nsub, nsub - 1);
-    const uint32_t pos = atomicAdd(&cur[q], 1u);
-    store_key<KW>(K2, D.n, pos, key);
-    I2[pos] = I1[t];
-  }
-}
-
-// ------------------------------------------------------------ 6. leaves
-__device__ __forceinline__ bool keep_sum(double2 s, double eps) {
-  if (eps == 0.0) return s.x != 0.0 || s.y != 0.0;
-  return hypot(s.x, s.y) > eps;
-}
-
-__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// Decoupled look-back over leaves, run by one full warp: publish this leaf's
-// kept count, then scan predecessors 32 at a time (flag 1 = aggregate only,
-// 2 = inclusive prefix, 0 = not yet published) until an inclusive prefix is
-// found.  Returns the exclusive prefix (valid in every lane).
-__device__ uint64_t leaf_lookback(unsigned long long* status, uint32_t leaf, uint64_t agg) {
-  constexpr unsigned long long kAgg = 1ull << 62, kPre = 2ull << 62, kVal = (1ull << 62) - 1;
-  const int lane = threadIdx.x & 31;
-  if (leaf == 0) {
-    if (lane == 0) st_relaxed_gpu(&status[0], kPre | agg);
-    return 0;
-  }
-  if (lane == 0) st_relaxed_gpu(&status[leaf], kAgg | agg);
-  uint64_t excl = 0;
-  int64_t base = (int64_t)leaf - 1;
-  for (;;) {
-    const int64_t idx = base - lane;
-    const unsigned long long v = idx >= 0 ? ld_relaxed_gpu(&status[idx]) : kPre;
-    const unsigned f = (unsigned)(v >> 62);
-    const unsigned inc = __ballot_sync(0xffffffffu, f == 2);
-    const unsigned zero = __ballot_sync(0xffffffffu, f == 0);
-    const int first = inc ? __ffs(inc) - 1 : 32;  // nearest inclusive predecessor
-    const unsigned need = first == 32 ? 0xffffffffu : ((2u << first) - 1u);
-    if (zero & need) continue;  // a needed predecessor has not published yet
-    unsigned long long c = (lane <= first) ? (v & kVal) : 0ull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    excl += c;
-    if (first < 32) break;
-    base -= 32;
-  }
-  if (lane == 0) st_relaxed_gpu(&status[leaf], kPre | (excl + agg));
-  return excl;
-}
-
-#include "merge_leaves.cuh"
-
-// ============================================================== host side
-static inline int64_t align256(int64_t v) { return (v + 255) & ~(int64_t)255; }
-
-struct WsLayout {
-  int64_t split, bcount, bbase, bcursor, leaf_off, n_leaves, leaf_ctr, leaf_desc, leaf_status,
-      k1, i1, k2, i2, total;
-};
-
-static WsLayout ws_layout(const pl_merge_plan& P) {
-  WsLayout w{};
-  const int64_t KW = P.key_words, nb1 = P.n_buckets, n = P.n_items;
-  const int64_t max_leaves = nb1 * (int64_t)P.max_sub;
-  int64_t o = 0;
-  w.split = o; o = align256(o + 8 * KW * nb1);
-  w.bcount = o; o = align256(o + 4 * nb1);
-  w.bbase = o; o = align256(o + 4 * (nb1 + 1));
-  w.bcursor = o; o = align256(o + 4 * nb1);
-  w.leaf_off = o; o = align256(o + 4 * (nb1 + 1));
-  w.n_leaves = o; o = align256(o + 4);
-  w.leaf_ctr = o; o = align256(o + 4);
-  w.leaf_status = o; o = align256(o + 8 * max_leaves);
-  const int64_t ctl_end = o;  // everything above is zeroed per call
-  w.leaf_desc = o; o = align256(o + 16 * max_leaves);
-  w.k1 = o; o = align256(o + 8 * KW * n);
-  w.i1 = o; o = align256(o + 4 * n);
-  w.k2 = o; o = align256(o + 8 * KW * n);
-  w.i2 = o; o = align256(o + 4 * n);
-  w.total = o;
-  (void)ctl_end;
-  return w;
-}
-
-static void finish_plan(pl_merge_plan* P, const u64* masks /* z[W] then x[W] */) {
-  const int W = P->W;
-  int pos = 0, active = 0;
-  for (int s = 0; s < 2 * W; ++s) {
-    const u64 m = masks[s];
-    if (m == 0) {
-      P->seg_lo[s] = 0;
-      P->seg_len[s] = 0;
-      P->seg_pos[s] = pos;
-      continue;
-    }
-    const int lo = __builtin_ctzll(m), hi = 63 - __builtin_clzll(m);
-    P->seg_lo[s] = lo;
-    P->seg_len[s] = hi - lo + 1;
-    P->seg_pos[s] = pos;
-    pos += hi - lo + 1;
-    active |= 1 << (s < W ? s : s - W);
-  }
-  for (int s = 2 * W; s < PL_PLAN_MAX_SEG; ++s) P->seg_lo[s] = P->seg_len[s] = P->seg_pos[s] = 0;
-  P->key_bits = pos;
-  P->key_words = key_words_for_bits(pos > 0 ? pos : 1);
-  P->reserved[0] = active;
-  const int KW = P->key_words;
-  const int cap = leaf_cap_for(KW);
-  P->leaf_cap = cap;
-  P->leaf_target = cap / 3;  // headroom: sampled splitters vary bucket sizes
-  // one-CTA sample capacity: the sampler sorts in up to kSortSmemBytes
-  const int scap = std::min(8192, kSortSmemBytes / (8 * KW + 4));
-  const int64_t n = P->n_items;
-  int64_t nb1 = 1;
-  if (n > cap) {
-    nb1 = (n + P->leaf_target - 1) / P->leaf_target;
-    const int64_t nb_max = std::min<int64_t>(kMaxBuckets, scap / kSampleOversample);
-    if (nb1 > nb_max) nb1 = nb_max;
-    if (nb1 < 2) nb1 = 2;
-  }
-  P->n_buckets = (int)nb1;
-  P->n_samples = nb1 > 1 ? (int)std::min<int64_t>(n, std::min<int64_t>(scap, nb1 * kSampleOversample)) : 0;
-  // level-2 sample capacity bounds the sub-bucket count
-  // level-2 sample (one CTA, <= 160 KB): >= 8 samples per sub-bucket
-  const int s2cap = std::max(64, std::min(8192, (160 * 1024) / (8 * KW + 4)));
-  P->max_sub = std::max(1, std::min(1024, s2cap / 8));
-  P->reserved[1] = s2cap;
-  P->workspace_bytes = ws_layout(*P).total;
-}
-
-template <int W>
-__global__ void k_or_masks(const u64* __restrict__ x, const u64* __restrict__ z, int64_t ld,
-                           int64_t m, u64* out) {
-  u64 mz[W], mx[W];
-#pragma unroll
-  for (int w = 0; w < W; ++w) mz[w] = mx[w] = 0;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m;
-       t += (int64_t)gridDim.x * blockDim.x) {
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-      mz[w] |= z[w * ld + t];
-      mx[w] |= x[w * ld + t];
-    }
-  }
-#pragma unroll
-  for (int w = 0; w < W; ++w) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mz[w] |= __shfl_xor_sync(0xffffffffu, mz[w], o);
-      mx[w] |= __shfl_xor_sync(0xffffffffu, mx[w], o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-      if (mz[w]) atomicOr(&out[w], mz[w]);
-      if (mx[w]) atomicOr(&out[W + w], mx[w]);
-    }
-  }
-}
-
-template <int W>
-static int launch_masks(const u64* x, const u64* z, int64_t ld, int64_t m, u64* out,
-                        cudaStream_t st) {
-  if (m == 0) return PL_OK;
-  int64_t blocks = ceil_div(m, 256);
-  if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
-  StageTimer t_(st, "k_or_masks");
-  k_or_masks<W><<<(unsigned)blocks, 256, 0, st>>>(x, z, ld, m, out);
-  PLB_CHECK_LAUNCH("k_or_masks");
-  return PL_OK;
-}
-
-static int compute_masks(int W, const u64* x1, const u64* z1, int64_t ld1, int64_t m1,
-                         const u64* x2, const u64* z2, int64_t ld2, int64_t m2, u64* host_masks,
-                         cudaStream_t st) {
-  u64* dmask = nullptr;
-  PLB_CUDA(cudaMallocAsync((void**)&dmask, 2 * W * sizeof(u64), st));
-  PLB_CUDA(cudaMemsetAsync(dmask, 0, 2 * W * sizeof(u64), st));
-  int rc = PLB_DISPATCH_W(W, launch_masks, x1, z1, ld1, m1, dmask, st);
-  if (rc == PL_OK && x2) rc = PLB_DISPATCH_W(W, launch_masks, x2, z2, ld2, m2, dmask, st);
-  if (rc == PL_OK) {
-    PLB_CUDA(cudaMemcpyAsync(host_masks, dmask, 2 * W * sizeof(u64), cudaMemcpyDeviceToHost, st));
-  }
-  cudaFreeAsync(dmask, st);
-  PLB_CUDA(cudaStreamSynchronize(st));
-  return rc;
-}
-
-static Layout to_layout(const pl_merge_plan& P) {
-  Layout L{};
-  L.W = P.W;
-  L.KW = P.key_words;
-  L.active = (int)P.reserved[0];
-  for (int s = 0; s < PL_PLAN_MAX_SEG; ++s) {
-    L.lo[s] = P.seg_lo[s];
-    L.len[s] = P.seg_len[s];
-    L.pos[s] = P.seg_pos[s];
-  }
-  return L;
-}
-
-static Dims to_dims(const pl_merge_plan& P) {
-  Dims D{};
-  D.n = P.n_items;
-  D.ma = P.ma;
-  D.mb = P.mb;
-  D.n_space = P.n_items;
-  D.j0 = 0;
-  D.nb1 = P.n_buckets;
-  D.nsamp = P.n_samples;
-  D.leaf_cap = P.leaf_cap;
-  D.leaf_target = P.leaf_target;
-  D.max_sub = P.max_sub;
-  D.max_leaves = P.n_buckets * P.max_sub;
-  return D;
-}
-
-static Ctl to_ctl(const pl_merge_plan& P, void* ws) {
-  const WsLayout w = ws_layout(P);
-  uint8_t* b = (uint8_t*)ws;
-  Ctl C;
-  C.split = (u64*)(b + w.split);
-  C.bcount = (uint32_t*)(b + w.bcount);
-  C.bbase = (uint32_t*)(b + w.bbase);
-  C.bcursor = (uint32_t*)(b + w.bcursor);
-  C.leaf_off = (uint32_t*)(b + w.leaf_off);
-  C.n_leaves = (uint32_t*)(b + w.n_leaves);
-  C.leaf_ctr = (uint32_t*)(b + w.leaf_ctr);
-  C.leaf_desc = (uint4*)(b + w.leaf_desc);
-  C.leaf_status = (unsigned long long*)(b + w.leaf_status);
-  C.k1 = (u64*)(b + w.k1);
-  C.i1 = (uint32_t*)(b + w.i1);
-  C.k2 = (u64*)(b + w.k2);
-  C.i2 = (uint32_t*)(b + w.i2);
-  return C;
-}
-
-template <typename K>
-static int set_smem(K kern, size_t bytes) {
-  if (bytes > 48 * 1024) {
-    PLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  }
-  return PL_OK;
-}
-
-template <int W, int KW, int MODE>
-static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const OutP& O,
-                        cudaStream_t st) {
-  const Layout L = to_layout(P);
-  const Dims D = to_dims(P);
-  const Ctl C = to_ctl(P, ws);
-  const WsLayout wl = ws_layout(P);
-  PLB_CUDA(cudaMemsetAsync(ws, 0, (size_t)wl.leaf_desc, st));  // control region
-
-  // 1-2. splitters + counts
-  if (D.nb1 > 1) {
-    const size_t sm1 = (size_t)D.nsamp * (8 * KW + 4) + 16;
-    if (set_smem(k_sample<W, KW, MODE>, sm1)) return PL_ERR_CUDA;
-    StageTimer t_(st, "k_sample");
-    k_sample<W, KW, MODE><<<1, kLeafThreads, sm1, st>>>(L, D, S, C);
-    PLB_CHECK_LAUNCH("k_sample");
-  }
-  const size_t gsm = (size_t)8 * KW * D.nb1 + 8 * D.nb1 + 8 + (size_t)16 * W * kGenTB +
-                     (size_t)4 * kGenTB * kGenThreads + 64;
-  dim3 ggrid;
-  if (MODE == 0) ggrid = dim3((unsigned)ceil_div(D.ma, kGenThreads), (unsigned)ceil_div(D.mb, kGenTB));
-  else ggrid = dim3((unsigned)ceil_div(D.n, (int64_t)kGenThreads * kGenTB), 1);
-  if (ggrid.y > 65535) {
-    set_error("outer product: |B| too large for one call (%lld)", (long long)D.mb);
-    return PL_ERR_CAPACITY;
-  }
-  if (D.nb1 > 1) {
-    if (set_smem(k_count<W, KW, MODE>, gsm)) return PL_ERR_CUDA;
-    StageTimer t_(st, "k_count");
-    k_count<W, KW, MODE><<<ggrid, kGenThreads, gsm, st>>>(L, D, S, C);
-    PLB_CHECK_LAUNCH("k_count");
-  }
-  // 3. bucket bases / leaves
-  {
-    StageTimer t_(st, "k_buckets");
-    k_buckets<<<1, 1024, 0, st>>>(D, C, O.count);
-    PLB_CHECK_LAUNCH("k_buckets");
-  }
-  // 4. scatter
-  if (set_smem(k_scatter<W, KW, MODE>, gsm)) return PL_ERR_CUDA;
-  {
-    StageTimer t_(st, "k_scatter");
-    k_scatter<W, KW, MODE><<<ggrid, kGenThreads, gsm, st>>>(L, D, S, C);
-    PLB_CHECK_LAUNCH("k_scatter");
-  }
-  // 5. level-2 split of oversized buckets
-  const int s2cap = (int)P.reserved[1];
-  const size_t ssm = (size_t)s2cap * (8 * KW + 4) + 8 + (size_t)8 * KW * D.max_sub +
-                     (size_t)8 * D.max_sub + 64;
-  if (set_smem(k_split<KW>, ssm)) return PL_ERR_CUDA;
-  {
-    StageTimer t_(st, "k_split");
-    k_split<KW><<<D.nb1, kSplitThreads, ssm, st>>>(D, C, s2cap);
-    PLB_CHECK_LAUNCH("k_split");
-  }
-  // 6. leaves
-  const size_t lsm = leaf_smem_bytes(KW);
-  auto lk = k_leaves<W, KW, MODE>;
-  if (set_smem(lk, lsm)) return PL_ERR_CUDA;
-  const int grid = kLeafCtasPerSm * num_sms();
-  StageTimer t_(st, "k_leaves");
-  lk<<<grid, kLeafThreads2, lsm, st>>>(L, D, S, C, O);
-  PLB_CHECK_LAUNCH("k_leaves");
-  return PL_OK;
-}
-
-// ------------------------------------------------------ K7 multi-GPU stages
-// Record layout exchanged between ranks: KW key words then ik, (KW+1) u64.
-template <int KW>
-__global__ void k_pack(const Ctl C, int64_t n, u64* __restrict__ out) {
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x) {
-#pragma unroll
-    for (int d = 0; d < KW; ++d) out[t * (KW + 1) + d] = C.k1[d * n + t];
-    out[t * (KW + 1) + KW] = C.i1[t];
-  }
-}
-
-// counts [G][nbl] -> bucket totals, per-segment source offsets and
-// destination offsets inside the bucket (one CTA, nbl <= kMaxBuckets)
-__global__ void __launch_bounds__(1024)
-k_regroup_prep(const uint32_t* __restrict__ cnt, int G, int nbl, Ctl C, uint32_t* seg_src,
-               uint32_t* seg_dst) {
-  __shared__ uint32_t src_base[65];
-  if (threadIdx.x == 0) {
-    uint32_t acc = 0;
-    for (int s = 0; s < G; ++s) {
-      src_base[s] = acc;
-      for (int b = 0; b < nbl; ++b) acc += cnt[s * nbl + b];
-    }
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < nbl; b += blockDim.x) {
-    uint32_t in_bucket = 0;
-    for (int s = 0; s < G; ++s) {
-      seg_dst[s * nbl + b] = in_bucket;
-      in_bucket += cnt[s * nbl + b];
-    }
-    C.bcount[b] = in_bucket;
-  }
-  if (threadIdx.x < G) {
-    const int s = threadIdx.x;
-    uint32_t acc = src_base[s];
-    for (int b = 0; b < nbl; ++b) {
-      seg_src[s * nbl + b] = acc;
-      acc += cnt[s * nbl + b];
-    }
-  }
-}
-
-template <int KW>
-__global__ void k_regroup_copy(const u64* __restrict__ recv, const uint32_t* __restrict__ cnt,
-                               int nbl, const uint32_t* __restrict__ seg_src,
-                               const uint32_t* __restrict__ seg_dst, Ctl C, int64_t n) {
-  const int b = blockIdx.x, s = blockIdx.y;
-  const uint32_t c = cnt[s * nbl + b];
-  const uint64_t src = seg_src[s * nbl + b];
-  const uint64_t dst = (uint64_t)C.bbase[b] + seg_dst[s * nbl + b];
-  for (uint32_t t = threadIdx.x; t < c; t += blockDim.x) {
-    const u64* r = recv + (src + t) * (KW + 1);
-#pragma unroll
-    for (int d = 0; d < KW; ++d) C.k1[d * n + dst + t] = r[d];
-    C.i1[dst + t] = (uint32_t)r[KW];
-  }
-}
-
-static pl_merge_plan local_plan(const pl_merge_plan& P, int64_t n_local, int nb) {
-  pl_merge_plan Q = P;
-  Q.n_items = n_local;
-  Q.n_buckets = nb;
-  Q.workspace_bytes = ws_layout(Q).total + align256(8LL * 64 * nb);
-  return Q;
-}
-
-template <int W, int KW>
-static int run_partition(const pl_merge_plan& P, const SrcA& S, int64_t j0, int64_t j1, void* ws,
-                         void* send, uint32_t* counts_out, cudaStream_t st) {
-  const pl_merge_plan Q = local_plan(P, P.ma * (j1 - j0), P.n_buckets);
-  const Layout L = to_layout(Q);
-  Dims D = to_dims(Q);
-  D.n_space = P.n_items;
-  D.mb = j1 - j0;
-  D.j0 = j0;
-  const Ctl C = to_ctl(Q, ws);
-  const WsLayout wl = ws_layout(Q);
-  PLB_CUDA(cudaMemsetAsync(ws, 0, (size_t)wl.leaf_desc, st));
-  if (D.n > 0) {
-    if (D.nb1 > 1) {
-      const size_t sm1 = (size_t)D.nsamp * (8 * KW + 4) + 16;
-      if (set_smem(k_sample<W, KW, 0>, sm1)) return PL_ERR_CUDA;
-      StageTimer t_(st, "k_sample");
-      k_sample<W, KW, 0><<<1, kLeafThreads, sm1, st>>>(L, D, S, C);
-      PLB_CHECK_LAUNCH("k_sample");
-    }
-    const size_t gsm = (size_t)8 * KW * D.nb1 + 8 * D.nb1 + 8 + (size_t)16 * W * kGenTB +
-                       (size_t)4 * kGenTB * kGenThreads + 64;
-    const dim3 ggrid((unsigned)ceil_div(D.ma, kGenThreads), (unsigned)ceil_div(D.mb, kGenTB));
-    if (D.nb1 > 1) {
-      if (set_smem(k_count<W, KW, 0>, gsm)) return PL_ERR_CUDA;
-      StageTimer t_(st, "k_count");
-      k_count<W, KW, 0><<<ggrid, kGenThreads, gsm, st>>>(L, D, S, C);
-      PLB_CHECK_LAUNCH("k_count");
-    }
-    {
-      StageTimer t_(st, "k_buckets");
-      k_buckets<<<1, 1024, 0, st>>>(D, C, (int64_t*)(C.n_leaves + 2));
-      PLB_CHECK_LAUNCH("k_buckets");
-    }
-    if (set_smem(k_scatter<W, KW, 0>, gsm)) return PL_ERR_CUDA;
-    {
-      StageTimer t_(st, "k_scatter");
-      k_scatter<W, KW, 0><<<ggrid, kGenThreads, gsm, st>>>(L, D, S, C);
-      PLB_CHECK_LAUNCH("k_scatter");
-    }
-    StageTimer t_(st, "k_pack");
-    k_pack<KW><<<4 * num_sms(), 256, 0, st>>>(C, D.n, (u64*)send);
-    PLB_CHECK_LAUNCH("k_pack");
-  }
-  PLB_CUDA(cudaMemcpyAsync(counts_out, C.bcount, 4 * (size_t)D.nb1, cudaMemcpyDeviceToDevice, st));
-  return PL_OK;
-}
-
-template <int W, int KW>
-static int run_merge_received(const pl_merge_plan& P, const u64* recv, int64_t n_recv,
-                              const uint32_t* cnt, int G, int nbl, const SrcA& S, void* ws,
-                              const OutP& O, cudaStream_t st) {
-  const pl_merge_plan Q = local_plan(P, n_recv, nbl);
-  const Layout L = to_layout(Q);
-  Dims D = to_dims(Q);
-  D.n_space = P.n_items;
-  const Ctl C = to_ctl(Q, ws);
-  const WsLayout wl = ws_layout(Q);
-  uint32_t* seg_src = (uint32_t*)((uint8_t*)ws + wl.total);
-  uint32_t* seg_dst = seg_src + 64 * nbl;
-  PLB_CUDA(cudaMemsetAsync(ws, 0, (size_t)wl.leaf_desc, st));
-  PLB_CUDA(cudaMemsetAsync(O.count, 0, sizeof(int64_t), st));
-  if (n_recv == 0) return PL_OK;
-  {
-    StageTimer t_(st, "k_regroup");
-    k_regroup_prep<<<1, 1024, 0, st>>>(cnt, G, nbl, C, seg_src, seg_dst);
-    PLB_CHECK_LAUNCH("k_regroup_prep");
-    k_buckets<<<1, 1024, 0, st>>>(D, C, O.count);
-    PLB_CHECK_LAUNCH("k_buckets");
-    k_regroup_copy<KW><<<dim3((unsigned)nbl, (unsigned)G), 256, 0, st>>>(recv, cnt, nbl, seg_src,
-                                                                        seg_dst, C, n_recv);
-    PLB_CHECK_LAUNCH("k_regroup_copy");
-  }
-  const int s2cap = (int)P.reserved[1];
-  const size_t ssm = (size_t)s2cap * (8 * KW + 4) + 8 + (size_t)8 * KW * D.max_sub +
-                     (size_t)8 * D.max_sub + 64;
-  if (set_smem(k_split<KW>, ssm)) return PL_ERR_CUDA;
-  {
-    StageTimer t_(st, "k_split");
-    k_split<KW><<<D.nb1, kSplitThreads, ssm, st>>>(D, C, s2cap);
-    PLB_CHECK_LAUNCH("k_split");
-  }
-  const size_t lsm = leaf_smem_bytes(KW);
-  auto lk = k_leaves<W, KW, 0>;
-  if (set_smem(lk, lsm)) return PL_ERR_CUDA;
-  StageTimer t_(st, "k_leaves");
-  lk<<<kLeafCtasPerSm * num_sms(), kLeafThreads2, lsm, st>>>(L, D, S, C, O);
-  PLB_CHECK_LAUNCH("k_leaves");
-  return PL_OK;
-}
-
-template <int W>
-static int dispatch_partition(const pl_merge_plan& P, const SrcA& S, int64_t j0, int64_t j1,
-                              void* ws, void* send, uint32_t* counts, cudaStream_t st) {
-  switch (P.key_words) {
-    case 1: return run_partition<W, 1>(P, S, j0, j1, ws, send, counts, st);
-    case 2: return run_partition<W, 2>(P, S, j0, j1, ws, send, counts, st);
-    case 4: return run_partition<W, (W >= 2 ? 4 : 1)>(P, S, j0, j1, ws, send, counts, st);
-    case 8: return run_partition<W, (W >= 4 ? 8 : 1)>(P, S, j0, j1, ws, send, counts, st);
-    case 16: return run_partition<W, (W >= 8 ? 16 : 1)>(P, S, j0, j1, ws, send, counts, st);
-    default: return run_partition<W, (W >= 16 ? 32 : 1)>(P, S, j0, j1, ws, send, counts, st);
-  }
-}
-
-template <int W>
-static int dispatch_received(const pl_merge_plan& P, const u64* recv, int64_t n_recv,
-                             const uint32_t* cnt, int G, int nbl, const SrcA& S, void* ws,
-                             const OutP& O, cudaStream_t st) {
-  switch (P.key_words) {
-    case 1: return run_merge_received<W, 1>(P, recv, n_recv, cnt, G, nbl, S, ws, O, st);
-    case 2: return run_merge_received<W, 2>(P, recv, n_recv, cnt, G, nbl, S, ws, O, st);
-    case 4: return run_merge_received<W, (W >= 2 ? 4 : 1)>(P, recv, n_recv, cnt, G, nbl, S, ws, O, st);
-    case 8: return run_merge_received<W, (W >= 4 ? 8 : 1)>(P, recv, n_recv, cnt, G, nbl, S, ws, O, st);
-    case 16: return run_merge_received<W, (W >= 8 ? 16 : 1)>(P, recv, n_recv, cnt, G, nbl, S, ws, O, st);
-    default: return run_merge_received<W, (W >= 16 ? 32 : 1)>(P, recv, n_recv, cnt, G, nbl, S, ws, O, st);
-  }
-}
-
-template <int W, int MODE>
-static int dispatch_kw(const pl_merge_plan& P, const SrcA& S, void* ws, const OutP& O,
-                       cudaStream_t st) {
-  switch (P.key_words) {
-    case 1: return run_pipeline<W, 1, MODE>(P, S, ws, O, st);
-    case 2: return run_pipeline<W, 2, MODE>(P, S, ws, O, st);
-    case 4: if (W >= 2) return run_pipeline<W, (W >= 2 ? 4 : 1), MODE>(P, S, ws, O, st); break;
-    case 8: if (W >= 4) return run_pipeline<W, (W >= 4 ? 8 : 1), MODE>(P, S, ws, O, st); break;
-    case 16: if (W >= 8) return run_pipeline<W, (W >= 8 ? 16 : 1), MODE>(P, S, ws, O, st); break;
-    case 32: if (W >= 16) return run_pipeline<W, (W >= 16 ? 32 : 1), MODE>(P, S, ws, O, st); break;
-    default: break;
-  }
-  set_error("unsupported key width %d words", P.key_words);
-  return PL_ERR_ARG;
-}
-
-template <int W>
-static int run_outer(const pl_merge_plan& P, const SrcA& S, void* ws, const OutP& O,
-                     cudaStream_t st) {
-  return dispatch_kw<W, 0>(P, S, ws, O, st);
-}
-template <int W>
-static int run_sort(const pl_merge_plan& P, const SrcA& S, void* ws, const OutP& O,
-                    cudaStream_t st) {
-  return dispatch_kw<W, 1>(P, S, ws, O, st);
-}
-
+PLB_COMBINE_INSTANTIATE(extern, 1)
+PLB_COMBINE_INSTANTIATE(extern, 2)
+PLB_COMBINE_INSTANTIATE(extern, 4)
+PLB_COMBINE_INSTANTIATE(extern, 8)
+PLB_COMBINE_INSTANTIATE(extern, 16)
 }  // namespace plb
 
 using namespace plb;

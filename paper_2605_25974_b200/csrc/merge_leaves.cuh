@@ -227,7 +227,7 @@ __device__ __forceinline__ void leaf_publish(unsigned long long* status, uint32_
 // Warp-parallel look-back for a leaf whose aggregate is already published:
 // scan predecessors 32 at a time until the nearest inclusive prefix, then
 // publish this leaf's inclusive prefix.  Returns the exclusive prefix.
-__device__ uint64_t leaf_lookback_pub(unsigned long long* status, uint32_t leaf, uint64_t agg) {
+static __device__ uint64_t leaf_lookback_pub(unsigned long long* status, uint32_t leaf, uint64_t agg) {
   const int lane = threadIdx.x & 31;
   if (leaf == 0) return 0;
   uint64_t excl = 0;
