@@ -23,13 +23,13 @@
 //   4. k_scatter  : items -> bucket-contiguous buffer 1 (per-CTA reservation)
 //   5. k_split    : buckets larger than a shared-memory leaf are re-partitioned
 //                   by a CTA-local sample into sub-buckets (buffer 2)
-//   6. k_leaves   : per leaf (<= leaf_cap items in shared memory, otherwise
-//                   in place in global memory): bitonic sort by (key, ik),
-//                   detect runs of equal keys, sum each run's coefficients
+//   6. k_leaf_sort: per leaf (<= leaf_cap items in shared memory, otherwise
+//                   in place in global memory): sort by (key, ik), detect runs
+//                   of equal keys, sum each run's coefficients
 //                   a_c[i]*b_c[j]*i^k in raw-row order with numpy's reduceat
-//                   summation tree (one thread per run, bit-exact),
-//                   drop |sum| <= eps, and write the merged terms at the
-//                   position found by a decoupled look-back over leaves.
+//                   summation tree (one thread per run, bit-exact), drop
+//                   |sum| <= eps, write the kept (key, sum) compacted.
+//   7. scan of kept counts per leaf; 8. k_emit: stream the merged terms out.
 // Runs never straddle buckets (splitters compare keys only) and each run is
 // summed by one thread in ik order, so the output is bit-identical whatever
 // the bucket structure, CTA schedule or GPU count.
@@ -38,6 +38,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "scan.cuh"
 
 namespace plb {
 
@@ -48,6 +49,8 @@ constexpr int kSplitThreads = 512;
 constexpr int kSortSmemBytes = 200 * 1024;
 constexpr int kSampleOversample = 16;
 constexpr int kMaxBuckets = 2048;
+constexpr int kSplitTile = 4096;     // items per level-2 classification tile
+constexpr int kSplitTileThreads = 256;
 
 // ---------------------------------------------------------------- layout
 struct Layout {
@@ -64,7 +67,16 @@ struct Ctl {  // control arrays inside the workspace
   uint32_t* n_leaves;    // 1
   uint32_t* leaf_ctr;    // 1
   uint4* leaf_desc;      // max_leaves: (buffer 1|2, offset, size, 0)
-  unsigned long long* leaf_status;  // max_leaves
+  u64* split2;           // [nb1][KW][max_sub] level-2 splitters per bucket
+  uint32_t* sub_count;   // [nb1][max_sub] level-2 counts, then cursors
+  uint32_t* tile_off;    // nb1 + 1: first split tile of each bucket
+  uint32_t* n_tiles;     // 1
+  uint32_t* kept;         // max_leaves: merged terms per leaf
+  uint32_t* kprefix;      // max_leaves: exclusive prefix of kept
+  uint32_t* scan_scratch; // scan_scratch_words(max_leaves)
+  uint32_t* scan_total;   // 1: total merged terms
+  double2* sums;          // [n] run sums, compacted per leaf
+  uint32_t* rmap;         // emit range -> first leaf
   u64* k1;               // [KW][n] item keys, buffer 1
   uint32_t* i1;          // [n]
   u64* k2;               // buffer 2
@@ -585,11 +597,12 @@ __device__ __forceinline__ int leaves_for(uint32_t size, const Dims& D) {
 }
 
 static __global__ void __launch_bounds__(1024) k_buckets(Dims D, Ctl C, int64_t* out_count) {
-  __shared__ uint32_t wsum[32], wsum2[32];
-  __shared__ uint32_t carry, carry2;
+  __shared__ uint32_t wsum[32], wsum2[32], wsum3[32];
+  __shared__ uint32_t carry, carry2, carry3;
   if (threadIdx.x == 0) {
     carry = 0;
     carry2 = 0;
+    carry3 = 0;
     if (D.nb1 == 1) C.bcount[0] = (uint32_t)D.n;
     *C.leaf_ctr = 0;
     *out_count = 0;
@@ -600,52 +613,80 @@ static __global__ void __launch_bounds__(1024) k_buckets(Dims D, Ctl C, int64_t*
     const int b = base + threadIdx.x;
     const uint32_t v = b < D.nb1 ? C.bcount[b] : 0;
     const uint32_t nl = b < D.nb1 ? (uint32_t)leaves_for(v, D) : 0;
-    uint32_t a = v, c = nl;
+    const uint32_t nt = (b < D.nb1 && (int)v > D.leaf_cap) ? (v + kSplitTile - 1) / kSplitTile : 0;
+    uint32_t a = v, c = nl, e = nt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t ta = __shfl_up_sync(0xffffffffu, a, o);
       const uint32_t tc = __shfl_up_sync(0xffffffffu, c, o);
-      if (lane >= o) { a += ta; c += tc; }
+      const uint32_t te = __shfl_up_sync(0xffffffffu, e, o);
+      if (lane >= o) { a += ta; c += tc; e += te; }
     }
-    if (lane == 31) { wsum[wid] = a; wsum2[wid] = c; }
+    if (lane == 31) { wsum[wid] = a; wsum2[wid] = c; wsum3[wid] = e; }
     __syncthreads();
     if (wid == 0) {
-      uint32_t s = wsum[lane], s2 = wsum2[lane];
+      uint32_t s = wsum[lane], s2 = wsum2[lane], s3 = wsum3[lane];
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t t = __shfl_up_sync(0xffffffffu, s, o);
         const uint32_t t2 = __shfl_up_sync(0xffffffffu, s2, o);
-        if (lane >= o) { s += t; s2 += t2; }
+        const uint32_t t3 = __shfl_up_sync(0xffffffffu, s3, o);
+        if (lane >= o) { s += t; s2 += t2; s3 += t3; }
       }
       wsum[lane] = s;
       wsum2[lane] = s2;
+      wsum3[lane] = s3;
     }
     __syncthreads();
     const uint32_t ex = carry + (wid ? wsum[wid - 1] : 0) + a - v;
     const uint32_t ex2 = carry2 + (wid ? wsum2[wid - 1] : 0) + c - nl;
+    const uint32_t ex3 = carry3 + (wid ? wsum3[wid - 1] : 0) + e - nt;
     if (b < D.nb1) {
       C.bbase[b] = ex;
       C.bcursor[b] = ex;
       C.leaf_off[b] = ex2;
+      C.tile_off[b] = ex3;
     }
     __syncthreads();
     if (threadIdx.x == blockDim.x - 1) {
       carry = ex + v;
       carry2 = ex2 + nl;
+      carry3 = ex3 + nt;
     }
     __syncthreads();
   }
   if (threadIdx.x == 0) {
     C.bbase[D.nb1] = carry;
     C.leaf_off[D.nb1] = carry2;
+    C.tile_off[D.nb1] = carry3;
     *C.n_leaves = carry2;
+    *C.n_tiles = carry3;
   }
 }
 
+template <typename K>
+static int set_smem(K kern, size_t bytes) {
+  if (bytes > 48 * 1024) {
+    PLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  }
+  return PL_OK;
+}
+
 // -------------------------------------------------------------- 5. split
+// Level 2: buckets larger than a shared-memory leaf are cut into nsub
+// sub-buckets (leaves) by splitters from a bucket-local sample.
+//   k_split_prep    CTA per bucket: leaf descriptor of an unsplit bucket, or
+//                   sample + sort + nsub-1 splitters (C.split2)
+//   k_split_count   CTA per tile of kSplitTile items of a split bucket:
+//                   classify (binary search in shared memory), histogram,
+//                   add into the bucket's sub-bucket counts
+//   k_split_bases   CTA per bucket: scan of sub-bucket counts -> leaf
+//                   descriptors and scatter cursors
+//   k_split_scatter same tiles: classify again, reserve per (tile, sub-bucket)
+//                   ranges, write the items into buffer 2
 template <int KW>
 __global__ void __launch_bounds__(kSplitThreads)
-k_split(Dims D, Ctl C, int s2cap) {
+k_split_prep(Dims D, Ctl C, int s2cap) {
   extern __shared__ u64 sm[];
   const int b = blockIdx.x;
   const uint32_t size = C.bcount[b], base = C.bbase[b];
@@ -659,55 +700,161 @@ k_split(Dims D, Ctl C, int s2cap) {
   int ns = nsub * kSampleOversample;
   if (ns > s2cap) ns = s2cap;
   if ((uint32_t)ns > size) ns = (int)size;
-  // smem: sample keys [KW][ns] | sample idx [ns] | split [KW][nsub] | hist, cur [nsub]
   u64* SK = sm;
   uint32_t* SI = reinterpret_cast<uint32_t*>(SK + (int64_t)KW * ns);
-  u64* SP = reinterpret_cast<u64*>(SI + ns + (ns & 1));
-  uint32_t* hist = reinterpret_cast<uint32_t*>(SP + (int64_t)KW * nsub);
-  uint32_t* cur = hist + nsub;
   const u64* K1 = C.k1 + base;
-  const uint32_t* I1 = C.i1 + base;
   for (int s = threadIdx.x; s < ns; s += blockDim.x) {
     const int64_t r = ((2 * (int64_t)s + 1) * size) / (2 * (int64_t)ns);
 #pragma unroll
     for (int d = 0; d < KW; ++d) SK[d * ns + s] = K1[d * D.n + r];
     SI[s] = (uint32_t)s;
   }
-  for (int q = threadIdx.x; q < nsub; q += blockDim.x) hist[q] = 0;
   __syncthreads();
   bitonic_sort<KW>(SK, SI, ns, ns);
+  u64* SP = C.split2 + (int64_t)b * KW * D.max_sub;
   for (int q = 1 + threadIdx.x; q < nsub; q += blockDim.x) {
     const int src = (int)(((int64_t)q * ns) / nsub);
 #pragma unroll
-    for (int d = 0; d < KW; ++d) SP[d * nsub + (q - 1)] = SK[d * ns + src];
+    for (int d = 0; d < KW; ++d) SP[d * D.max_sub + (q - 1)] = SK[d * ns + src];
   }
-  __syncthreads();
-  for (uint32_t t = threadIdx.x; t < size; t += blockDim.x) {
-    u64 key[KW];
-    load_key<KW>(K1, D.n, t, key);
-    atomicAdd(&hist[bucket_of<KW>(key, SP, nsub, nsub - 1)], 1u);
+}
+
+// tile t -> its bucket (last b with tile_off[b] <= t)
+__device__ __forceinline__ int tile_bucket(const Ctl& C, int nb1, uint32_t t) {
+  int lo = 0, hi = nb1 - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (C.tile_off[mid] <= t) lo = mid;
+    else hi = mid - 1;
   }
+  return lo;
+}
+
+struct SplitTile {
+  int b, nsub;
+  uint32_t base, size, t0, t1;  // bucket base/size; item range [t0, t1) inside the bucket
+};
+
+// loads the tile's bucket splitters into shared memory; false if no tile
+template <int KW>
+__device__ __forceinline__ bool split_tile_setup(const Dims& D, const Ctl& C, u64* SP,
+                                                 uint32_t* hist, SplitTile& T) {
+  __shared__ int s_b;
+  const uint32_t t = blockIdx.x;
+  if (t >= *C.n_tiles) return false;
+  if (threadIdx.x == 0) s_b = tile_bucket(C, D.nb1, t);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t acc = 0;
-    for (int q = 0; q < nsub; ++q) {
-      const uint32_t h = hist[q];
-      cur[q] = acc;
-      C.leaf_desc[lo + q] = make_uint4(2u, base + acc, h, 0u);
-      acc += h;
+  T.b = s_b;
+  T.base = C.bbase[T.b];
+  T.size = C.bcount[T.b];
+  T.nsub = leaves_for(T.size, D);
+  T.t0 = (t - C.tile_off[T.b]) * kSplitTile;
+  T.t1 = min(T.size, T.t0 + kSplitTile);
+  const u64* G = C.split2 + (int64_t)T.b * KW * D.max_sub;
+  for (int q = threadIdx.x; q < T.nsub; q += blockDim.x) {
+    hist[q] = 0;
+    if (q < T.nsub - 1) {
+#pragma unroll
+      for (int d = 0; d < KW; ++d) SP[d * D.max_sub + q] = G[d * D.max_sub + q];
     }
   }
   __syncthreads();
-  u64* K2 = C.k2 + base;
-  uint32_t* I2 = C.i2 + base;
-  for (uint32_t t = threadIdx.x; t < size; t += blockDim.x) {
+  return true;
+}
+
+template <int KW>
+__global__ void __launch_bounds__(kSplitTileThreads)
+k_split_count(Dims D, Ctl C) {
+  extern __shared__ u64 sm[];
+  u64* SP = sm;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(SP + (int64_t)KW * D.max_sub);
+  SplitTile T;
+  if (!split_tile_setup<KW>(D, C, SP, hist, T)) return;
+  const u64* K1 = C.k1 + T.base;
+  for (uint32_t t = T.t0 + threadIdx.x; t < T.t1; t += kSplitTileThreads) {
     u64 key[KW];
     load_key<KW>(K1, D.n, t, key);
-    const int q = bucket_of<KW>(key, SP, nsub, nsub - 1);
-    const uint32_t pos = atomicAdd(&cur[q], 1u);
-    store_key<KW>(K2, D.n, pos, key);
-    I2[pos] = I1[t];
+    atomicAdd(&hist[bucket_of<KW>(key, SP, D.max_sub, T.nsub - 1)], 1u);
   }
+  __syncthreads();
+  uint32_t* g = C.sub_count + (int64_t)T.b * D.max_sub;
+  for (int q = threadIdx.x; q < T.nsub; q += kSplitTileThreads)
+    if (hist[q]) atomicAdd(&g[q], hist[q]);
+}
+
+static __global__ void __launch_bounds__(1024) k_split_bases(Dims D, Ctl C) {
+  const int b = blockIdx.x;
+  const uint32_t size = C.bcount[b];
+  if ((int)size <= D.leaf_cap) return;
+  const uint32_t base = C.bbase[b], lo = C.leaf_off[b];
+  const int nsub = leaves_for(size, D);
+  uint32_t* g = C.sub_count + (int64_t)b * D.max_sub;
+  uint32_t carry = 0;
+  for (int q0 = 0; q0 < nsub; q0 += blockDim.x) {
+    const int q = q0 + threadIdx.x;
+    const uint32_t h = q < nsub ? g[q] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan(h, &tot) + carry;
+    if (q < nsub) {
+      C.leaf_desc[lo + q] = make_uint4(2u, base + ex, h, 0u);
+      g[q] = base + ex;  // cursor
+    }
+    carry += tot;
+  }
+}
+
+template <int KW>
+__global__ void __launch_bounds__(kSplitTileThreads)
+k_split_scatter(Dims D, Ctl C) {
+  extern __shared__ u64 sm[];
+  u64* SP = sm;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(SP + (int64_t)KW * D.max_sub);
+  uint32_t* gbase = hist + D.max_sub;
+  uint32_t* code = gbase + D.max_sub;  // per item: sub << 16 | rank
+  SplitTile T;
+  if (!split_tile_setup<KW>(D, C, SP, hist, T)) return;
+  const u64* K1 = C.k1 + T.base;
+  const uint32_t* I1 = C.i1 + T.base;
+  for (uint32_t t = T.t0 + threadIdx.x; t < T.t1; t += kSplitTileThreads) {
+    u64 key[KW];
+    load_key<KW>(K1, D.n, t, key);
+    const int q = bucket_of<KW>(key, SP, D.max_sub, T.nsub - 1);
+    code[t - T.t0] = ((uint32_t)q << 16) | atomicAdd(&hist[q], 1u);
+  }
+  __syncthreads();
+  uint32_t* g = C.sub_count + (int64_t)T.b * D.max_sub;
+  for (int q = threadIdx.x; q < T.nsub; q += kSplitTileThreads)
+    if (hist[q]) gbase[q] = atomicAdd(&g[q], hist[q]);
+  __syncthreads();
+  for (uint32_t t = T.t0 + threadIdx.x; t < T.t1; t += kSplitTileThreads) {
+    const uint32_t cd = code[t - T.t0];
+    const uint32_t pos = gbase[cd >> 16] + (cd & 0xFFFFu);
+    u64 key[KW];
+    load_key<KW>(K1, D.n, t, key);
+    store_key<KW>(C.k2, D.n, pos, key);
+    C.i2[pos] = I1[t];
+  }
+}
+
+template <int KW>
+static int launch_split(const pl_merge_plan& P, const Dims& D, const Ctl& C, cudaStream_t st) {
+  const int s2cap = (int)P.reserved[1];
+  const size_t psm = (size_t)s2cap * (8 * KW + 4) + 16;
+  if (set_smem(k_split_prep<KW>, psm)) return PL_ERR_CUDA;
+  const size_t tsm = (size_t)8 * KW * D.max_sub + 8 * (size_t)D.max_sub + 4 * (size_t)kSplitTile + 64;
+  if (set_smem(k_split_count<KW>, tsm)) return PL_ERR_CUDA;
+  if (set_smem(k_split_scatter<KW>, tsm)) return PL_ERR_CUDA;
+  const unsigned max_tiles = (unsigned)(ceil_div(D.n, (int64_t)kSplitTile) + D.nb1);
+  StageTimer t_(st, "k_split");
+  k_split_prep<KW><<<D.nb1, kSplitThreads, psm, st>>>(D, C, s2cap);
+  PLB_CHECK_LAUNCH("k_split_prep");
+  k_split_count<KW><<<max_tiles, kSplitTileThreads, tsm, st>>>(D, C);
+  PLB_CHECK_LAUNCH("k_split_count");
+  k_split_bases<<<D.nb1, 1024, 0, st>>>(D, C);
+  PLB_CHECK_LAUNCH("k_split_bases");
+  k_split_scatter<KW><<<max_tiles, kSplitTileThreads, tsm, st>>>(D, C);
+  PLB_CHECK_LAUNCH("k_split_scatter");
+  return PL_OK;
 }
 
 // ------------------------------------------------------------ 6. leaves
@@ -725,48 +872,14 @@ __device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned l
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Decoupled look-back over leaves, run by one full warp: publish this leaf's
-// kept count, then scan predecessors 32 at a time (flag 1 = aggregate only,
-// 2 = inclusive prefix, 0 = not yet published) until an inclusive prefix is
-// found.  Returns the exclusive prefix (valid in every lane).
-static __device__ uint64_t leaf_lookback(unsigned long long* status, uint32_t leaf, uint64_t agg) {
-  constexpr unsigned long long kAgg = 1ull << 62, kPre = 2ull << 62, kVal = (1ull << 62) - 1;
-  const int lane = threadIdx.x & 31;
-  if (leaf == 0) {
-    if (lane == 0) st_relaxed_gpu(&status[0], kPre | agg);
-    return 0;
-  }
-  if (lane == 0) st_relaxed_gpu(&status[leaf], kAgg | agg);
-  uint64_t excl = 0;
-  int64_t base = (int64_t)leaf - 1;
-  for (;;) {
-    const int64_t idx = base - lane;
-    const unsigned long long v = idx >= 0 ? ld_relaxed_gpu(&status[idx]) : kPre;
-    const unsigned f = (unsigned)(v >> 62);
-    const unsigned inc = __ballot_sync(0xffffffffu, f == 2);
-    const unsigned zero = __ballot_sync(0xffffffffu, f == 0);
-    const int first = inc ? __ffs(inc) - 1 : 32;  // nearest inclusive predecessor
-    const unsigned need = first == 32 ? 0xffffffffu : ((2u << first) - 1u);
-    if (zero & need) continue;  // a needed predecessor has not published yet
-    unsigned long long c = (lane <= first) ? (v & kVal) : 0ull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    excl += c;
-    if (first < 32) break;
-    base -= 32;
-  }
-  if (lane == 0) st_relaxed_gpu(&status[leaf], kPre | (excl + agg));
-  return excl;
-}
-
 #include "merge_leaves.cuh"
 
 // ============================================================== host side
 static inline int64_t align256(int64_t v) { return (v + 255) & ~(int64_t)255; }
 
 struct WsLayout {
-  int64_t split, bcount, bbase, bcursor, leaf_off, n_leaves, leaf_ctr, leaf_desc, leaf_status,
-      k1, i1, k2, i2, total;
+  int64_t split, bcount, bbase, bcursor, leaf_off, n_leaves, leaf_ctr, tile_off, n_tiles,
+      sub_count, leaf_desc, split2, kept, kprefix, scan, k1, i1, k2, i2, sums, rmap, total;
 };
 
 static WsLayout ws_layout(const pl_merge_plan& P) {
@@ -781,13 +894,21 @@ static WsLayout ws_layout(const pl_merge_plan& P) {
   w.leaf_off = o; o = align256(o + 4 * (nb1 + 1));
   w.n_leaves = o; o = align256(o + 4);
   w.leaf_ctr = o; o = align256(o + 4);
-  w.leaf_status = o; o = align256(o + 8 * max_leaves);
+  w.tile_off = o; o = align256(o + 4 * (nb1 + 1));
+  w.n_tiles = o; o = align256(o + 4);
+  w.sub_count = o; o = align256(o + 4 * max_leaves);
   const int64_t ctl_end = o;  // everything above is zeroed per call
   w.leaf_desc = o; o = align256(o + 16 * max_leaves);
+  w.split2 = o; o = align256(o + 8 * KW * max_leaves);
+  w.kept = o; o = align256(o + 4 * max_leaves);
+  w.kprefix = o; o = align256(o + 4 * max_leaves);
+  w.scan = o; o = align256(o + 4 * (scan_scratch_words(max_leaves) + 1));
   w.k1 = o; o = align256(o + 8 * KW * n);
   w.i1 = o; o = align256(o + 4 * n);
   w.k2 = o; o = align256(o + 8 * KW * n);
   w.i2 = o; o = align256(o + 4 * n);
+  w.sums = o; o = align256(o + 16 * n);
+  w.rmap = o; o = align256(o + 4 * (n / 128 + 2));
   w.total = o;
   (void)ctl_end;
   return w;
@@ -936,7 +1057,16 @@ static Ctl to_ctl(const pl_merge_plan& P, void* ws) {
   C.n_leaves = (uint32_t*)(b + w.n_leaves);
   C.leaf_ctr = (uint32_t*)(b + w.leaf_ctr);
   C.leaf_desc = (uint4*)(b + w.leaf_desc);
-  C.leaf_status = (unsigned long long*)(b + w.leaf_status);
+  C.split2 = (u64*)(b + w.split2);
+  C.sub_count = (uint32_t*)(b + w.sub_count);
+  C.tile_off = (uint32_t*)(b + w.tile_off);
+  C.n_tiles = (uint32_t*)(b + w.n_tiles);
+  C.kept = (uint32_t*)(b + w.kept);
+  C.kprefix = (uint32_t*)(b + w.kprefix);
+  C.scan_scratch = (uint32_t*)(b + w.scan);
+  C.scan_total = C.scan_scratch + scan_scratch_words(P.n_buckets * (int64_t)P.max_sub);
+  C.sums = (double2*)(b + w.sums);
+  C.rmap = (uint32_t*)(b + w.rmap);
   C.k1 = (u64*)(b + w.k1);
   C.i1 = (uint32_t*)(b + w.i1);
   C.k2 = (u64*)(b + w.k2);
@@ -944,13 +1074,6 @@ static Ctl to_ctl(const pl_merge_plan& P, void* ws) {
   return C;
 }
 
-template <typename K>
-static int set_smem(K kern, size_t bytes) {
-  if (bytes > 48 * 1024) {
-    PLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  }
-  return PL_OK;
-}
 
 template <int W, int KW, int MODE>
 static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const OutP& O,
@@ -998,24 +1121,12 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const O
     PLB_CHECK_LAUNCH("k_scatter");
   }
   // 5. level-2 split of oversized buckets
-  const int s2cap = (int)P.reserved[1];
-  const size_t ssm = (size_t)s2cap * (8 * KW + 4) + 8 + (size_t)8 * KW * D.max_sub +
-                     (size_t)8 * D.max_sub + 64;
-  if (set_smem(k_split<KW>, ssm)) return PL_ERR_CUDA;
   {
-    StageTimer t_(st, "k_split");
-    k_split<KW><<<D.nb1, kSplitThreads, ssm, st>>>(D, C, s2cap);
-    PLB_CHECK_LAUNCH("k_split");
+    const int rc = launch_split<KW>(P, D, C, st);
+    if (rc) return rc;
   }
-  // 6. leaves
-  const size_t lsm = leaf_smem_bytes(KW);
-  auto lk = k_leaves<W, KW, MODE>;
-  if (set_smem(lk, lsm)) return PL_ERR_CUDA;
-  const int grid = kLeafCtasPerSm * num_sms();
-  StageTimer t_(st, "k_leaves");
-  lk<<<grid, kLeafThreads2, lsm, st>>>(L, D, S, C, O);
-  PLB_CHECK_LAUNCH("k_leaves");
-  return PL_OK;
+  // 6. leaves: sort + reduce, scan, emit
+  return launch_leaves<W, KW, MODE>(L, D, S, C, O, st);
 }
 
 // ------------------------------------------------------ K7 multi-GPU stages
@@ -1159,22 +1270,11 @@ static int run_merge_received(const pl_merge_plan& P, const u64* recv, int64_t n
                                                                         seg_dst, C, n_recv);
     PLB_CHECK_LAUNCH("k_regroup_copy");
   }
-  const int s2cap = (int)P.reserved[1];
-  const size_t ssm = (size_t)s2cap * (8 * KW + 4) + 8 + (size_t)8 * KW * D.max_sub +
-                     (size_t)8 * D.max_sub + 64;
-  if (set_smem(k_split<KW>, ssm)) return PL_ERR_CUDA;
   {
-    StageTimer t_(st, "k_split");
-    k_split<KW><<<D.nb1, kSplitThreads, ssm, st>>>(D, C, s2cap);
-    PLB_CHECK_LAUNCH("k_split");
+    const int rc = launch_split<KW>(P, D, C, st);
+    if (rc) return rc;
   }
-  const size_t lsm = leaf_smem_bytes(KW);
-  auto lk = k_leaves<W, KW, 0>;
-  if (set_smem(lk, lsm)) return PL_ERR_CUDA;
-  StageTimer t_(st, "k_leaves");
-  lk<<<kLeafCtasPerSm * num_sms(), kLeafThreads2, lsm, st>>>(L, D, S, C, O);
-  PLB_CHECK_LAUNCH("k_leaves");
-  return PL_OK;
+  return launch_leaves<W, KW, 0>(L, D, S, C, O, st);
 }
 
 template <int W>

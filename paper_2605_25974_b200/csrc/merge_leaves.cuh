@@ -1,22 +1,18 @@
-// Leaf stage of the merge pipeline (included by combine.cu, which defines the
-// key helpers, RunSum, Source, keep_sum and the relaxed gpu-scope loads).
+// Leaf stage of the merge pipeline (included by combine_impl.cuh, which
+// defines the key helpers, RunSum, Source and keep_sum).
 //
-// Persistent CTAs of kLeafThreads2 threads (4 per SM) take leaves in order
-// from an atomic counter.  Each leaf (<= leaf_cap items, staged in shared
-// memory) goes through two phases, software-pipelined over two buffers so a
-// CTA never idles waiting for a predecessor:
-//   phase A (leaf i):  load; bitonic sort by (key, ik) -- stages whose blocks
-//       fit in one warp's contiguous segment run warp-synchronously; run heads;
-//       pass 1 sums each run in numpy reduceat order (RunSum) and keeps those
-//       with |sum| > eps; a block scan fills POS[q] = head of kept run q; the
-//       kept count is published as the leaf's aggregate.
-//   phase B (leaf i, after phase A of leaf i+1):  warp-parallel decoupled
-//       look-back -> global output base; publish the inclusive prefix; pass 2
-//       writes merged term q from thread q (coalesced plane stores),
-//       recomputing the run sum.
+//   k_leaf_sort  one CTA per leaf (<= leaf_cap items staged in shared memory):
+//                radix sort on a 24-bit key window below the leaf's common
+//                prefix, ties finished on the full (key, ik) (bitonic network
+//                when a tie segment is long); run heads; each run summed in
+//                numpy reduceat order by one thread (RunSum); |sum| <= eps
+//                dropped; kept (key, sum) written compacted at the leaf's
+//                offset in the idle item buffer + C.sums; kept count per leaf.
+//   k_leaf_scan  exclusive scan of the kept counts -> output offset per leaf.
+//   k_emit       warp per leaf: unpack each kept key into the 2W plane words
+//                and write the SoA output term (planes, phase 0, coefficient).
 // Leaves larger than leaf_cap (one key repeated more than leaf_cap times,
-// which no splitter can divide) are sorted in place in global memory and
-// processed synchronously, tile by tile.
+// which no splitter can divide) are sorted in place in global memory.
 #pragma once
 
 // Shared-memory items per leaf buffer for key width KW (two buffers of about
@@ -25,13 +21,22 @@ __host__ __device__ constexpr int leaf_cap_for(int KW) {
   return KW <= 2 ? 1024 : KW == 4 ? 512 : KW == 8 ? 256 : KW == 16 ? 128 : 64;
 }
 
-__host__ __device__ constexpr size_t leaf_smem_bytes(int KW) {
-  return 2 * (((size_t)leaf_cap_for(KW) * (8 * KW + 4 + 2 + 1) + 15) & ~(size_t)15) + 64;
+__host__ __device__ constexpr size_t leaf_buf_stride(int KW) {
+  return ((size_t)leaf_cap_for(KW) * (8 * KW + 4 + 2 + 1) + 15) & ~(size_t)15;
 }
 
 constexpr int kLeafThreads2 = 256;
-constexpr int kLeafCtasPerSm = 3;  // 85 registers per thread, no spills in the hot path
 constexpr int kLeafWarps2 = kLeafThreads2 / 32;
+constexpr int kRadixBits = 8, kRadixBins = 1 << kRadixBits, kRadixPasses = 3;
+constexpr int kRadixWindow = kRadixBits * kRadixPasses;
+constexpr int kRadixTieMax = 32;
+
+__host__ __device__ constexpr size_t radix_smem_bytes(int cap) {
+  // window keys x2 | perm x2 (u16) | per-warp bin counters (u16)
+  return (size_t)cap * 4 * 2 + (size_t)cap * 2 * 2 + (size_t)kLeafWarps2 * kRadixBins * 2 + 16;
+}
+
+
 
 template <int KW>
 __device__ __forceinline__ void cmp_swap(u64* K, uint32_t* I, int64_t stride, int i, int p) {
@@ -128,7 +133,7 @@ __device__ __forceinline__ void bitonic_fixed(u64* K, uint32_t* I, int n) {
 // Bitonic sort of n items in shared memory with warp-local stages
 // (STRIDE = leaf capacity, a compile-time constant).
 template <int KW, int STRIDE>
-__device__ void bitonic_sort_local(u64* K, uint32_t* I, int n) {
+__device__ __noinline__ void bitonic_sort_local(u64* K, uint32_t* I, int n) {
   int npow = 1;
   while (npow < n) npow <<= 1;
   switch (npow) {
@@ -201,6 +206,189 @@ __device__ __forceinline__ uint32_t leaf_excl_scan(uint32_t v, uint32_t* s_warp,
   return before + inc - v;
 }
 
+// ---------------------------------------------------------------- leaf radix sort
+// The items of one leaf lie in a narrow key range, so after the bits they all
+// share, a 24-bit window starting at their highest differing bit orders them
+// almost completely.  The leaf is sorted by that window with a stable LSD
+// radix sort (3 passes of 8 bits, warp multisplit with match.any), then every
+// segment of equal windows is finished by an insertion sort on the full
+// (key, ik); a segment longer than kRadixTieMax (many equal keys) makes the
+// caller fall back to the bitonic network.  Result: identical order to the
+// bitonic sort, about a tenth of its shared-memory traffic.
+
+
+// bits [p, p + kRadixWindow) of the key (bit 0 = MSB of word 0), zero-padded
+template <int KW>
+__device__ __forceinline__ uint32_t key_window(const u64* K, int stride, int t, int p) {
+  const int d = p >> 6, o = p & 63;
+  const u64 hi = K[d * stride + t];
+  const u64 lo = d + 1 < KW ? K[(d + 1) * stride + t] : 0ull;
+  const u64 v = o ? ((hi << o) | (lo >> (64 - o))) : hi;
+  return (uint32_t)(v >> (64 - kRadixWindow));
+}
+
+template <int KW, int CAP>
+__device__ __noinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint8_t* scratch) {
+  constexpr int SEG = CAP / kLeafWarps2;             // max positions owned by one warp
+  constexpr int SLOTS = SEG >= 32 ? SEG / 32 : 1;
+  // only the first npos positions take part: warps own seg = npos / 8 each
+  const int npos = SEG >= 32 ? (n + kLeafThreads2 - 1) / kLeafThreads2 * kLeafThreads2 : CAP;
+  const int seg = SEG >= 32 ? npos / kLeafWarps2 : SEG;
+  const int slots = SEG >= 32 ? seg / 32 : 1;
+  uint32_t* wk[2] = {reinterpret_cast<uint32_t*>(scratch),
+                     reinterpret_cast<uint32_t*>(scratch) + CAP};
+  uint16_t* wp[2] = {reinterpret_cast<uint16_t*>(scratch + 8 * CAP),
+                     reinterpret_cast<uint16_t*>(scratch + 8 * CAP) + CAP};
+  uint16_t* hist = reinterpret_cast<uint16_t*>(scratch + 12 * CAP);  // [warp][bin]
+  __shared__ u64 s_or[kLeafWarps2][KW];
+  __shared__ int s_flag;
+  __shared__ uint32_t s_scan[kLeafWarps2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // 1. highest bit at which any key differs from item 0
+  u64 acc[KW];
+#pragma unroll
+  for (int d = 0; d < KW; ++d) acc[d] = 0;
+  for (int t = tid; t < n; t += kLeafThreads2) {
+#pragma unroll
+    for (int d = 0; d < KW; ++d) acc[d] |= K[d * CAP + t] ^ K[d * CAP];
+  }
+#pragma unroll
+  for (int d = 0; d < KW; ++d) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[d] |= __shfl_xor_sync(0xffffffffu, acc[d], o);
+    if (lane == 0) s_or[warp][d] = acc[d];
+  }
+  if (tid == 0) s_flag = 0;
+  __syncthreads();
+  int p = -1;
+#pragma unroll
+  for (int d = KW - 1; d >= 0; --d) {
+    u64 v = 0;
+#pragma unroll
+    for (int w = 0; w < kLeafWarps2; ++w) v |= s_or[w][d];
+    if (v) p = d * 64 + __clzll(v);
+  }
+  if (p < 0) return false;  // every key equal: order is by ik alone (bitonic)
+
+  // 2. window keys in position order; positions >= n sort last (stable, max key)
+  for (int t = tid; t < npos; t += kLeafThreads2) {
+    wk[0][t] = t < n ? key_window<KW>(K, CAP, t, p) : 0xFFFFFFFFu >> (32 - kRadixWindow);
+    wp[0][t] = (uint16_t)t;
+  }
+  __syncthreads();
+
+  // 3. LSD passes; warp w owns positions [w*seg, (w+1)*seg), slot-major
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const bool lane_on = SEG >= 32 || lane < SEG;
+  int cur = 0;
+#pragma unroll 1
+  for (int pass = 0; pass < kRadixPasses; ++pass) {
+    const int sh = pass * kRadixBits;
+    uint16_t* hw = hist + warp * kRadixBins;
+    for (int b = lane; b < kRadixBins; b += 32) hw[b] = 0;
+    __syncwarp();
+    uint32_t key[SLOTS];
+    uint16_t pm[SLOTS], rk[SLOTS];
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      const int pos = warp * seg + s * 32 + lane;
+      if (lane_on && s < slots) {
+        key[s] = wk[cur][pos];
+        pm[s] = wp[cur][pos];
+        const uint32_t dg = (key[s] >> sh) & (kRadixBins - 1);
+        const unsigned grp = __match_any_sync(SEG >= 32 ? 0xffffffffu : ((1u << SEG) - 1u), dg);
+        const uint16_t prev = hw[dg];
+        __syncwarp(SEG >= 32 ? 0xffffffffu : ((1u << SEG) - 1u));
+        if ((grp & lt_mask) == 0) hw[dg] = (uint16_t)(prev + __popc(grp));
+        __syncwarp(SEG >= 32 ? 0xffffffffu : ((1u << SEG) - 1u));
+        rk[s] = (uint16_t)(prev + __popc(grp & lt_mask));
+      }
+    }
+    __syncthreads();
+    // bin-major offsets: bin b's start, then warps in order inside the bin
+    {
+      uint32_t tot = 0;
+      for (int b = tid; b < kRadixBins; b += kLeafThreads2)
+        for (int w = 0; w < kLeafWarps2; ++w) tot += hist[w * kRadixBins + b];
+      uint32_t all;
+      uint32_t run = leaf_excl_scan(tid < kRadixBins ? tot : 0u, s_scan, &all);
+      if (tid < kRadixBins) {
+#pragma unroll
+        for (int w = 0; w < kLeafWarps2; ++w) {
+          const uint16_t c = hist[w * kRadixBins + tid];
+          hist[w * kRadixBins + tid] = (uint16_t)run;
+          run += c;
+        }
+      }
+    }
+    __syncthreads();
+    if (lane_on) {
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s) {
+        if (s >= slots) break;
+        const uint32_t dg = (key[s] >> sh) & (kRadixBins - 1);
+        const int np = hw[dg] + rk[s];
+        wk[cur ^ 1][np] = key[s];
+        wp[cur ^ 1][np] = pm[s];
+      }
+    }
+    cur ^= 1;
+    __syncthreads();
+  }
+
+  // 4. finish segments of equal windows on the full (key, ik)
+  const uint32_t* sk = wk[cur];
+  uint16_t* sp = wp[cur];
+  for (int q = tid; q < n; q += kLeafThreads2) {
+    if ((q > 0 && sk[q - 1] == sk[q]) || q + 1 >= n || sk[q + 1] != sk[q]) continue;
+    int e = q + 1;
+    while (e < n && sk[e] == sk[q] && e - q <= kRadixTieMax) ++e;
+    if (e - q > kRadixTieMax) {
+      s_flag = 1;
+      continue;
+    }
+    for (int a = q + 1; a < e; ++a) {  // insertion sort of sp[q..e)
+      const uint16_t v = sp[a];
+      int b = a;
+      while (b > q && item_lt<KW>(K, I, CAP, v, sp[b - 1])) {
+        sp[b] = sp[b - 1];
+        --b;
+      }
+      sp[b] = v;
+    }
+  }
+  __syncthreads();
+  if (s_flag) return false;
+
+  // 5. gather K, I into sorted order in place
+  constexpr int PER = (CAP + kLeafThreads2 - 1) / kLeafThreads2;
+  u64 gk[PER][KW];
+  uint32_t gi[PER];
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    const int t = r * kLeafThreads2 + tid;
+    if (t < n) {
+      const int src = sp[t];
+#pragma unroll
+      for (int d = 0; d < KW; ++d) gk[r][d] = K[d * CAP + src];
+      gi[r] = I[src];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    const int t = r * kLeafThreads2 + tid;
+    if (t < n) {
+#pragma unroll
+      for (int d = 0; d < KW; ++d) K[d * CAP + t] = gk[r][d];
+      I[t] = gi[r];
+    }
+  }
+  __syncthreads();
+  return true;
+}
+
 template <int W, int KW>
 __device__ __forceinline__ void write_term(const Layout& L, const OutP& O, uint64_t pos,
                                            const u64 (&key)[KW], double2 s) {
@@ -215,213 +403,281 @@ __device__ __forceinline__ void write_term(const Layout& L, const OutP& O, uint6
   O.oc[pos] = s;
 }
 
-constexpr unsigned long long kLbAgg = 1ull << 62, kLbPre = 2ull << 62,
-                             kLbVal = (1ull << 62) - 1;
-
-// Publish a leaf's kept count (inclusive prefix for leaf 0).
-__device__ __forceinline__ void leaf_publish(unsigned long long* status, uint32_t leaf,
-                                             uint64_t agg) {
-  st_relaxed_gpu(&status[leaf], (leaf == 0 ? kLbPre : kLbAgg) | agg);
-}
-
-// Warp-parallel look-back for a leaf whose aggregate is already published:
-// scan predecessors 32 at a time until the nearest inclusive prefix, then
-// publish this leaf's inclusive prefix.  Returns the exclusive prefix.
-static __device__ uint64_t leaf_lookback_pub(unsigned long long* status, uint32_t leaf, uint64_t agg) {
-  const int lane = threadIdx.x & 31;
-  if (leaf == 0) return 0;
-  uint64_t excl = 0;
-  int64_t base = (int64_t)leaf - 1;
-  for (;;) {
-    const int64_t idx = base - lane;
-    const unsigned long long v = idx >= 0 ? ld_relaxed_gpu(&status[idx]) : kLbPre;
-    const unsigned f = (unsigned)(v >> 62);
-    const unsigned inc = __ballot_sync(0xffffffffu, f == 2);
-    const unsigned zero = __ballot_sync(0xffffffffu, f == 0);
-    const int first = inc ? __ffs(inc) - 1 : 32;
-    const unsigned need = first == 32 ? 0xffffffffu : ((2u << first) - 1u);
-    if (zero & need) continue;
-    unsigned long long c = (lane <= first) ? (v & kLbVal) : 0ull;
+// ------------------------------------------------------------ leaf sort
+// One CTA per leaf (grid = the plan's leaf bound; CTAs past n_leaves record an
+// empty leaf).  Load the leaf's items into shared memory, sort by (key, ik),
+// mark run heads, sum each run in numpy reduceat order (RunSum, one thread per
+// run), drop |sum| <= eps, and write the kept runs compacted -- key words to
+// the idle item buffer at the leaf's own offset, sums to C.sums -- plus the
+// leaf's kept count.  Leaves larger than the shared-memory capacity (one key
+// repeated more than leaf_cap times) are sorted in place in global memory.
+// Oversized leaf (one key repeated more than leaf_cap times): bitonic sort in
+// place in global memory, then tiles of kLeafThreads2*8 items.  Returns the
+// kept count (valid in thread 0).
+template <int W, int KW, int MODE>
+__device__ __noinline__ uint32_t leaf_sort_global(const Dims& D, const SrcA& S, const u64* GK,
+                                                  const uint32_t* GI, u64* DK, double2* DS,
+                                                  int n, double eps, uint32_t* s_warp) {
+  using RS = RunSum<W, KW, MODE>;
+  const int tid = threadIdx.x;
+    u64* K = const_cast<u64*>(GK);
+    uint32_t* I = const_cast<uint32_t*>(GI);
+    const int64_t stride = D.n;
+    bitonic_sort<KW>(K, I, stride, n);
+    const int tile = kLeafThreads2 * 8;
+    uint32_t base = 0;
+    for (int t0 = 0; t0 < n; t0 += tile) {
+      uint32_t mine = 0;
+      for (int p = t0 + tid * 8; p < min(n, t0 + tid * 8 + 8); ++p) {
+        if (p != 0 && key_eq<KW>(K, stride, p, p - 1)) continue;
+        int q = p + 1;
+        while (q < n && key_eq<KW>(K, stride, q, q - 1)) ++q;
+        if (keep_sum(RS::run(S, D.ma, I, p, q - p), eps)) ++mine;
+      }
+      uint32_t tt;
+      uint32_t pos = base + leaf_excl_scan(mine, s_warp, &tt);
+      for (int p = t0 + tid * 8; p < min(n, t0 + tid * 8 + 8); ++p) {
+        if (p != 0 && key_eq<KW>(K, stride, p, p - 1)) continue;
+        int q = p + 1;
+        while (q < n && key_eq<KW>(K, stride, q, q - 1)) ++q;
+        const double2 s = RS::run(S, D.ma, I, p, q - p);
+        if (keep_sum(s, eps)) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    excl += c;
-    if (first < 32) break;
-    base -= 32;
-  }
-  if (lane == 0) st_relaxed_gpu(&status[leaf], kLbPre | (excl + agg));
-  return excl;
+          for (int d = 0; d < KW; ++d) DK[d * stride + pos] = K[d * stride + p];
+          DS[pos] = s;
+          ++pos;
+        }
+      }
+      base += tt;
+    }
+  return base;
 }
 
-template <int KW>
-struct LeafBuf {
-  u64* K;         // [KW][cap]
-  uint32_t* I;    // [cap]
-  uint16_t* POS;  // [cap]
-  uint8_t* HEAD;  // [cap]
-};
+constexpr int kSortCtasPerSm = 4;
 
+template <int W, int KW, int MODE>
+__global__ void __launch_bounds__(kLeafThreads2, kSortCtasPerSm)
+k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
+  extern __shared__ u64 sm[];
+  constexpr int cap = leaf_cap_for(KW);  // == D.leaf_cap
+  __shared__ uint32_t s_warp[kLeafWarps2];
+  const int tid = threadIdx.x;
+  const uint32_t leaf = blockIdx.x;
+  if (leaf >= *C.n_leaves) {
+    if (tid == 0) C.kept[leaf] = 0;
+    return;
+  }
+  using RS = RunSum<W, KW, MODE>;
+  const uint4 dsc = C.leaf_desc[leaf];
+  const int n = (int)dsc.z;
+  const uint32_t off = dsc.y;
+  const u64* GK = (dsc.x == 1 ? C.k1 : C.k2) + off;
+  const uint32_t* GI = (dsc.x == 1 ? C.i1 : C.i2) + off;
+  u64* DK = (dsc.x == 1 ? C.k2 : C.k1) + off;  // idle buffer at the same offset
+  double2* DS = C.sums + off;
+
+  if (n > cap) {
+    const uint32_t kept = leaf_sort_global<W, KW, MODE>(D, S, GK, GI, DK, DS, n, eps, s_warp);
+    if (tid == 0) C.kept[leaf] = kept;
+    return;
+  }
+
+  // shared memory: K [KW][cap] | I [cap] | POS u16 [cap] | HEAD u8 [cap] | scratch
+  u64* K = sm;
+  uint32_t* I = reinterpret_cast<uint32_t*>(K + (int64_t)KW * cap);
+  uint16_t* POS = reinterpret_cast<uint16_t*>(I + cap);
+  uint8_t* HEAD = reinterpret_cast<uint8_t*>(POS + cap);
+  uint8_t* scratch = reinterpret_cast<uint8_t*>(sm) + leaf_buf_stride(KW);
+  double2* SUM = reinterpret_cast<double2*>(scratch);  // reuses the radix scratch
+  for (int t = tid; t < n; t += kLeafThreads2) {
+#pragma unroll
+    for (int d = 0; d < KW; ++d) K[d * cap + t] = GK[d * D.n + t];
+    I[t] = GI[t];
+  }
+  __syncthreads();
+  if (n > 1 && !radix_sort_leaf<KW, cap>(K, I, n, scratch)) bitonic_sort_local<KW, cap>(K, I, n);
+  for (int p = tid; p < n; p += kLeafThreads2)
+    HEAD[p] = (p == 0 || !key_eq<KW>(K, cap, p, p - 1)) ? 1 : 0;
+  __syncthreads();
+  const int ch = (n + kLeafThreads2 - 1) / kLeafThreads2;  // <= 8
+  const int p0 = tid * ch, p1 = min(n, p0 + ch);
+  uint32_t keepbits = 0;
+  for (int p = p0; p < p1; ++p) {
+    if (!HEAD[p]) continue;
+    int q = p + 1;
+    while (q < n && !HEAD[q]) ++q;
+    const double2 s = RS::run(S, D.ma, I, p, q - p);
+    if (keep_sum(s, eps)) {
+      keepbits |= 1u << (p - p0);
+      SUM[p] = s;
+    }
+  }
+  uint32_t kept;
+  uint32_t slot = leaf_excl_scan(__popc(keepbits), s_warp, &kept);
+  for (uint32_t bb = keepbits; bb; bb &= bb - 1) POS[slot++] = (uint16_t)(p0 + __ffs(bb) - 1);
+  __syncthreads();
+  for (uint32_t q = tid; q < kept; q += kLeafThreads2) {
+    const int p = POS[q];
+#pragma unroll
+    for (int d = 0; d < KW; ++d) DK[d * D.n + q] = K[d * cap + p];
+    DS[q] = SUM[p];
+  }
+  if (tid == 0) C.kept[leaf] = kept;
+}
+
+__host__ __device__ constexpr size_t leaf_sort_smem_bytes(int KW) {
+  return leaf_buf_stride(KW) + radix_smem_bytes(leaf_cap_for(KW)) + 64;
+}
+
+// ------------------------------------------------------------ emit
+// Streams the merged terms out in output order: a CTA owns the output range
+// [o0, o0 + T) (T = emit_tile(KW) terms), finds the leaves covering it
+// (binary search on the kept-count prefix), stages the range's (key, sum)
+// entries in shared memory, then writes the SoA output one plane at a time --
+// each plane store of the CTA is T*8 contiguous bytes, aligned, so every
+// DRAM sector is written whole exactly once.
+constexpr int kEmitThreads = 256;
+__host__ __device__ constexpr int emit_tile(int KW) {
+  return KW <= 2 ? 2048 : KW <= 4 ? 1024 : KW <= 8 ? 512 : KW <= 16 ? 256 : 128;
+}
+__host__ __device__ constexpr size_t emit_smem_bytes(int KW) {
+  return (size_t)emit_tile(KW) * (8 * KW + 16) + (size_t)kEmitThreads * 12 + 64;
+}
+
+// last leaf l in [lo, hi] with pre[l] <= v (pre non-decreasing, pre[lo] <= v)
+__device__ __forceinline__ uint32_t leaf_at(const uint32_t* pre, uint32_t lo, uint32_t hi,
+                                            uint32_t v) {
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= v) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// rmap[r] = the leaf holding output position r*T (every position lies in
+// exactly one leaf with kept > 0)
 template <int KW>
-__device__ __forceinline__ LeafBuf<KW> leaf_buf(u64* sm, int cap, int b) {
-  const size_t bytes = (size_t)cap * (8 * KW + 4 + 2 + 1);
-  const size_t stride = (bytes + 15) & ~(size_t)15;
-  uint8_t* base = reinterpret_cast<uint8_t*>(sm) + b * stride;
-  LeafBuf<KW> lb;
-  lb.K = reinterpret_cast<u64*>(base);
-  lb.I = reinterpret_cast<uint32_t*>(lb.K + (int64_t)KW * cap);
-  lb.POS = reinterpret_cast<uint16_t*>(lb.I + cap);
-  lb.HEAD = reinterpret_cast<uint8_t*>(lb.POS + cap);
-  return lb;
+__global__ void k_range_map(Dims D, Ctl C) {
+  constexpr uint32_t T = emit_tile(KW);
+  const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= *C.n_leaves) return;
+  const uint32_t k = C.kept[l];
+  if (k == 0) return;
+  const uint32_t pre = C.kprefix[l];
+  for (uint32_t r = (pre + T - 1) / T; r * T < pre + k; ++r) C.rmap[r] = l;
+}
+
+template <int W, int KW>
+__global__ void __launch_bounds__(kEmitThreads)
+k_emit(Layout L, Dims D, Ctl C, OutP O) {
+  constexpr int T = emit_tile(KW);
+  constexpr int PER = T / kEmitThreads;
+  extern __shared__ u64 sm[];
+  u64* KS = sm;                                              // [KW][T]
+  double2* SS = reinterpret_cast<double2*>(KS + (int64_t)KW * T);  // [T]
+  uint32_t* m_pre = reinterpret_cast<uint32_t*>(SS + T);     // leaf chunk metadata
+  uint32_t* m_end = m_pre + kEmitThreads;
+  uint32_t* m_src = m_end + kEmitThreads;                    // buffer << 31 | offset
+  const int tid = threadIdx.x;
+  const uint32_t n_leaves = *C.n_leaves;
+  const uint32_t total = *C.scan_total;
+  if (blockIdx.x == 0 && tid == 0) *O.count = (int64_t)total;
+  for (uint64_t o0 = (uint64_t)blockIdx.x * T; o0 < total; o0 += (uint64_t)gridDim.x * T) {
+    const uint32_t o1 = (uint32_t)(o0 + T < total ? o0 + T : total);
+    const uint32_t r = (uint32_t)(o0 / T);
+    const uint32_t l0 = C.rmap[r];
+    const uint32_t l1 = o1 < total ? C.rmap[r + 1] : n_leaves - 1;
+    for (uint32_t lb = l0; lb <= l1; lb += kEmitThreads) {
+      const uint32_t nl = l1 - lb + 1 < (uint32_t)kEmitThreads ? l1 - lb + 1 : (uint32_t)kEmitThreads;
+      if (tid < (int)nl) {
+        const uint32_t l = lb + tid;
+        const uint4 dsc = C.leaf_desc[l];
+        const uint32_t pre = C.kprefix[l];
+        m_pre[tid] = pre;
+        m_end[tid] = pre + C.kept[l];
+        m_src[tid] = (dsc.x == 1 ? 0x80000000u : 0u) | dsc.y;  // kept entries live in the idle buffer
+      }
+      __syncthreads();
+      const uint32_t c_lo = m_pre[0], c_hi = m_end[nl - 1];
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const uint32_t p = (uint32_t)o0 + u * kEmitThreads + tid;
+        if (p >= o1 || p < c_lo || p >= c_hi) continue;
+        const uint32_t j = leaf_at(m_pre, 0, nl - 1, p);
+        if (p >= m_end[j]) continue;  // (cannot happen: leaves tile the output)
+        const uint32_t src = m_src[j];
+        const u64* SK = ((src >> 31) ? C.k2 : C.k1) + (src & 0x7FFFFFFFu) + (p - m_pre[j]);
+        const int e = u * kEmitThreads + tid;
+#pragma unroll
+        for (int d = 0; d < KW; ++d) KS[d * T + e] = __ldg(SK + d * D.n);
+        SS[e] = __ldg(C.sums + (src & 0x7FFFFFFFu) + (p - m_pre[j]));
+      }
+      __syncthreads();
+    }
+    // plane-major stores: each plane gets T*8 contiguous bytes from this CTA
+    for (int q = 0; q < 2 * W; ++q) {
+      const int len = L.len[q];
+      u64* dst = (q < W ? O.oz + (int64_t)q * O.ldo : O.ox + (int64_t)(q - W) * O.ldo) + o0;
+      const int pos = L.pos[q], lo = L.lo[q];
+      const int wi = pos >> 6, off = pos & 63;
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int e = u * kEmitThreads + tid;
+        if ((uint32_t)o0 + e >= o1) break;
+        u64 w = 0;
+        if (len) {
+          const u64 a = KS[wi * T + e];
+          const u64 b = (off && wi + 1 < KW) ? KS[(wi + 1) * T + e] : 0ull;
+          const u64 hi = off ? ((a << off) | (b >> (64 - off))) : a;
+          w = (hi >> (64 - len)) << lo;
+        }
+        dst[e] = w;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = u * kEmitThreads + tid;
+      if ((uint32_t)o0 + e >= o1) break;
+      O.oc[o0 + e] = SS[e];
+    }
+    for (int e = tid * 4; e < T; e += kEmitThreads * 4) {
+      if ((uint32_t)o0 + e + 4 <= o1 && ((o0 + e) & 3) == 0 &&
+          (reinterpret_cast<uintptr_t>(O.ok + o0 + e) & 3) == 0) {
+        *reinterpret_cast<uint32_t*>(O.ok + o0 + e) = 0u;
+      } else {
+        for (int f = e; f < e + 4 && (uint32_t)o0 + f < o1; ++f) O.ok[o0 + f] = 0;
+      }
+    }
+    __syncthreads();
+  }
 }
 
 template <int W, int KW, int MODE>
-__global__ void __launch_bounds__(kLeafThreads2, kLeafCtasPerSm)
-k_leaves(Layout L, Dims D, SrcA S, Ctl C, OutP O) {
-  extern __shared__ u64 sm[];
-  constexpr int cap = leaf_cap_for(KW);  // == D.leaf_cap
-  __shared__ uint32_t s_leaf;
-  __shared__ uint32_t s_warp[kLeafWarps2];
-  __shared__ uint64_t s_base;
-  const int tid = threadIdx.x;
-  const uint32_t n_leaves = *C.n_leaves;
-  using RS = RunSum<W, KW, MODE>;
-
-  // pending phase-B work
-  bool have_prev = false;
-  uint32_t prev_leaf = 0, prev_kept = 0;
-  int prev_n = 0, prev_buf = 0, cur = 0;
-
-  auto phase_b = [&](uint32_t leaf, uint32_t kept, int n, int b) {
-    const LeafBuf<KW> B = leaf_buf<KW>(sm, cap, b);
-    if (tid < 32) {
-      const uint64_t excl = leaf_lookback_pub(C.leaf_status, leaf, kept);
-      if (tid == 0) {
-        s_base = excl;
-        if (leaf == n_leaves - 1) *O.count = (int64_t)(excl + kept);
-      }
-    }
-    __syncthreads();
-    const uint64_t base = s_base;
-    for (uint32_t q = tid; q < kept; q += kLeafThreads2) {
-      const int p = B.POS[q];
-      int e = p + 1;
-      while (e < n && !B.HEAD[e]) ++e;
-      const double2 s = RS::run(S, D.ma, B.I, p, e - p);
-      u64 key[KW];
-      load_key<KW>(B.K, cap, p, key);
-      write_term<W, KW>(L, O, base + q, key, s);
-    }
-    __syncthreads();
-  };
-
-  for (;;) {
-    if (tid == 0) s_leaf = atomicAdd(C.leaf_ctr, 1u);
-    __syncthreads();
-    const uint32_t leaf = s_leaf;
-    const bool done = leaf >= n_leaves;
-    if (!done) {
-      const uint4 dsc = C.leaf_desc[leaf];
-      const int n = (int)dsc.z;
-      const u64* GK = (dsc.x == 1 ? C.k1 : C.k2) + dsc.y;
-      const uint32_t* GI = (dsc.x == 1 ? C.i1 : C.i2) + dsc.y;
-      if (n > cap) {
-        // ---------------------------------- oversized leaf, synchronous
-        if (have_prev) {
-          phase_b(prev_leaf, prev_kept, prev_n, prev_buf);
-          have_prev = false;
-        }
-        u64* K = const_cast<u64*>(GK);
-        uint32_t* I = const_cast<uint32_t*>(GI);
-        const int64_t stride = D.n;
-        bitonic_sort<KW>(K, I, stride, n);
-        const int tile = kLeafThreads2 * 8;
-        uint32_t total = 0;
-        for (int t0 = 0; t0 < n; t0 += tile) {
-          uint32_t mine = 0;
-          for (int p = t0 + tid * 8; p < min(n, t0 + tid * 8 + 8); ++p) {
-            if (p != 0 && key_eq<KW>(K, stride, p, p - 1)) continue;
-            int q = p + 1;
-            while (q < n && key_eq<KW>(K, stride, q, q - 1)) ++q;
-            if (keep_sum(RS::run(S, D.ma, I, p, q - p), O.eps)) ++mine;
-          }
-          uint32_t tt;
-          leaf_excl_scan(mine, s_warp, &tt);
-          total += tt;
-        }
-        if (tid < 32) {
-          if (tid == 0) leaf_publish(C.leaf_status, leaf, total);
-          __syncwarp();
-          const uint64_t excl = leaf_lookback_pub(C.leaf_status, leaf, total);
-          if (tid == 0) {
-            s_base = excl;
-            if (leaf == n_leaves - 1) *O.count = (int64_t)(excl + total);
-          }
-        }
-        __syncthreads();
-        uint64_t base = s_base;
-        for (int t0 = 0; t0 < n; t0 += tile) {
-          uint32_t mine = 0;
-          for (int p = t0 + tid * 8; p < min(n, t0 + tid * 8 + 8); ++p) {
-            if (p != 0 && key_eq<KW>(K, stride, p, p - 1)) continue;
-            int q = p + 1;
-            while (q < n && key_eq<KW>(K, stride, q, q - 1)) ++q;
-            if (keep_sum(RS::run(S, D.ma, I, p, q - p), O.eps)) ++mine;
-          }
-          uint32_t tt;
-          uint64_t pos = base + leaf_excl_scan(mine, s_warp, &tt);
-          for (int p = t0 + tid * 8; p < min(n, t0 + tid * 8 + 8); ++p) {
-            if (p != 0 && key_eq<KW>(K, stride, p, p - 1)) continue;
-            int q = p + 1;
-            while (q < n && key_eq<KW>(K, stride, q, q - 1)) ++q;
-            const double2 s = RS::run(S, D.ma, I, p, q - p);
-            if (keep_sum(s, O.eps)) {
-              u64 key[KW];
-              load_key<KW>(K, stride, p, key);
-              write_term<W, KW>(L, O, pos++, key, s);
-            }
-          }
-          base += tt;
-        }
-        __syncthreads();
-        continue;
-      }
-      // -------------------------------------------- phase A (buffer cur)
-      const LeafBuf<KW> B = leaf_buf<KW>(sm, cap, cur);
-      for (int t = tid; t < n; t += kLeafThreads2) {
-#pragma unroll
-        for (int d = 0; d < KW; ++d) B.K[d * cap + t] = GK[d * D.n + t];
-        B.I[t] = GI[t];
-      }
-      __syncthreads();
-      if (n > 1) bitonic_sort_local<KW, cap>(B.K, B.I, n);
-      for (int p = tid; p < n; p += kLeafThreads2)
-        B.HEAD[p] = (p == 0 || !key_eq<KW>(B.K, cap, p, p - 1)) ? 1 : 0;
-      __syncthreads();
-      const int ch = (n + kLeafThreads2 - 1) / kLeafThreads2;  // <= 8
-      const int p0 = tid * ch, p1 = min(n, p0 + ch);
-      uint32_t keepbits = 0;
-      for (int p = p0; p < p1; ++p) {
-        if (!B.HEAD[p]) continue;
-        int q = p + 1;
-        while (q < n && !B.HEAD[q]) ++q;
-        if (keep_sum(RS::run(S, D.ma, B.I, p, q - p), O.eps)) keepbits |= 1u << (p - p0);
-      }
-      uint32_t kept;
-      uint32_t slot = leaf_excl_scan(__popc(keepbits), s_warp, &kept);
-      for (uint32_t bb = keepbits; bb; bb &= bb - 1) B.POS[slot++] = (uint16_t)(p0 + __ffs(bb) - 1);
-      if (tid == 0) leaf_publish(C.leaf_status, leaf, kept);
-      __syncthreads();
-      // ------------------------------- phase B of the previous leaf
-      if (have_prev) phase_b(prev_leaf, prev_kept, prev_n, prev_buf);
-      have_prev = true;
-      prev_leaf = leaf;
-      prev_kept = kept;
-      prev_n = n;
-      prev_buf = cur;
-      cur ^= 1;
-    } else {
-      if (have_prev) phase_b(prev_leaf, prev_kept, prev_n, prev_buf);
-      break;
-    }
+static int launch_leaves(const Layout& L, const Dims& D, const SrcA& S, const Ctl& C,
+                         const OutP& O, cudaStream_t st) {
+  const size_t lsm = leaf_sort_smem_bytes(KW);
+  auto ks = k_leaf_sort<W, KW, MODE>;
+  if (lsm > 48 * 1024)
+    PLB_CUDA(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+  {
+    StageTimer t_(st, "k_leaf_sort");
+    ks<<<(unsigned)D.max_leaves, kLeafThreads2, lsm, st>>>(L, D, S, C, O.eps);
+    PLB_CHECK_LAUNCH("k_leaf_sort");
   }
+  {
+    StageTimer t_(st, "k_leaf_scan");
+    int rc = exclusive_scan_u32(C.kept, C.kprefix, D.max_leaves, C.scan_scratch, C.scan_total, st);
+    if (rc) return rc;
+  }
+  k_range_map<KW><<<(unsigned)ceil_div(D.max_leaves, 256), 256, 0, st>>>(D, C);
+  PLB_CHECK_LAUNCH("k_range_map");
+  const size_t esm = emit_smem_bytes(KW);
+  auto ke = k_emit<W, KW>;
+  if (esm > 48 * 1024)
+    PLB_CUDA(cudaFuncSetAttribute(ke, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm));
+  StageTimer t_(st, "k_emit");
+  ke<<<(unsigned)(3 * num_sms()), kEmitThreads, esm, st>>>(L, D, C, O);
+  PLB_CHECK_LAUNCH("k_emit");
+  return PL_OK;
 }
-
