@@ -35,6 +35,8 @@
 // the bucket structure, CTA schedule or GPU count.
 #pragma once
 #include <algorithm>
+#include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -1000,19 +1002,35 @@ static int launch_masks(const u64* x, const u64* z, int64_t ld, int64_t m, u64* 
   return PL_OK;
 }
 
+// OR-masks of the operands' words (the plan's key layout).  One small
+// device + pinned host buffer per device, reused under a lock, so planning
+// costs one tiny kernel and one stream sync (no allocation per call).
 static int compute_masks(int W, const u64* x1, const u64* z1, int64_t ld1, int64_t m1,
                          const u64* x2, const u64* z2, int64_t ld2, int64_t m2, u64* host_masks,
                          cudaStream_t st) {
-  u64* dmask = nullptr;
-  PLB_CUDA(cudaMallocAsync((void**)&dmask, 2 * W * sizeof(u64), st));
+  static std::mutex mtx;
+  static u64* dbuf[64] = {nullptr};
+  static u64* hbuf[64] = {nullptr};
+  int dev = 0;
+  PLB_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) {
+    set_error("device index %d out of range", dev);
+    return PL_ERR_ARG;
+  }
+  std::lock_guard<std::mutex> lock(mtx);
+  if (!dbuf[dev]) {
+    PLB_CUDA(cudaMalloc((void**)&dbuf[dev], 2 * PL_PLAN_MAX_SEG * sizeof(u64)));
+    PLB_CUDA(cudaMallocHost((void**)&hbuf[dev], 2 * PL_PLAN_MAX_SEG * sizeof(u64)));
+  }
+  u64* dmask = dbuf[dev];
   PLB_CUDA(cudaMemsetAsync(dmask, 0, 2 * W * sizeof(u64), st));
   int rc = PLB_DISPATCH_W(W, launch_masks, x1, z1, ld1, m1, dmask, st);
   if (rc == PL_OK && x2) rc = PLB_DISPATCH_W(W, launch_masks, x2, z2, ld2, m2, dmask, st);
   if (rc == PL_OK) {
-    PLB_CUDA(cudaMemcpyAsync(host_masks, dmask, 2 * W * sizeof(u64), cudaMemcpyDeviceToHost, st));
+    PLB_CUDA(cudaMemcpyAsync(hbuf[dev], dmask, 2 * W * sizeof(u64), cudaMemcpyDeviceToHost, st));
   }
-  cudaFreeAsync(dmask, st);
   PLB_CUDA(cudaStreamSynchronize(st));
+  if (rc == PL_OK) memcpy(host_masks, hbuf[dev], 2 * W * sizeof(u64));
   return rc;
 }
 

@@ -18,14 +18,14 @@
 // Shared-memory items per leaf buffer for key width KW (two buffers of about
 // 23 KB per CTA so four CTAs fit on one SM).
 __host__ __device__ constexpr int leaf_cap_for(int KW) {
-  return KW <= 2 ? 1024 : KW == 4 ? 512 : KW == 8 ? 256 : KW == 16 ? 128 : 64;
+  return KW <= 2 ? 512 : KW == 4 ? 256 : KW == 8 ? 128 : KW == 16 ? 64 : 32;
 }
 
 __host__ __device__ constexpr size_t leaf_buf_stride(int KW) {
   return ((size_t)leaf_cap_for(KW) * (8 * KW + 4 + 2 + 1) + 15) & ~(size_t)15;
 }
 
-constexpr int kLeafThreads2 = 256;
+constexpr int kLeafThreads2 = 128;
 constexpr int kLeafWarps2 = kLeafThreads2 / 32;
 constexpr int kRadixBits = 8, kRadixBins = 1 << kRadixBits, kRadixPasses = 3;
 constexpr int kRadixWindow = kRadixBits * kRadixPasses;
@@ -306,18 +306,25 @@ __device__ __noinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint8_t
       }
     }
     __syncthreads();
-    // bin-major offsets: bin b's start, then warps in order inside the bin
+    // bin-major offsets: bin b's start, then warps in order inside the bin;
+    // thread t owns the BPT consecutive bins [t*BPT, (t+1)*BPT)
     {
+      constexpr int BPT = kRadixBins / kLeafThreads2;
+      static_assert(BPT >= 1 && BPT * kLeafThreads2 == kRadixBins, "bins per thread");
       uint32_t tot = 0;
-      for (int b = tid; b < kRadixBins; b += kLeafThreads2)
-        for (int w = 0; w < kLeafWarps2; ++w) tot += hist[w * kRadixBins + b];
+#pragma unroll
+      for (int i = 0; i < BPT; ++i)
+#pragma unroll
+        for (int w = 0; w < kLeafWarps2; ++w) tot += hist[w * kRadixBins + tid * BPT + i];
       uint32_t all;
-      uint32_t run = leaf_excl_scan(tid < kRadixBins ? tot : 0u, s_scan, &all);
-      if (tid < kRadixBins) {
+      uint32_t run = leaf_excl_scan(tot, s_scan, &all);
+#pragma unroll
+      for (int i = 0; i < BPT; ++i) {
 #pragma unroll
         for (int w = 0; w < kLeafWarps2; ++w) {
-          const uint16_t c = hist[w * kRadixBins + tid];
-          hist[w * kRadixBins + tid] = (uint16_t)run;
+          const int h = w * kRadixBins + tid * BPT + i;
+          const uint16_t c = hist[h];
+          hist[h] = (uint16_t)run;
           run += c;
         }
       }
@@ -453,7 +460,7 @@ __device__ __noinline__ uint32_t leaf_sort_global(const Dims& D, const SrcA& S, 
   return base;
 }
 
-constexpr int kSortCtasPerSm = 4;
+constexpr int kSortCtasPerSm = 8;
 
 template <int W, int KW, int MODE>
 __global__ void __launch_bounds__(kLeafThreads2, kSortCtasPerSm)
@@ -499,7 +506,7 @@ k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
   for (int p = tid; p < n; p += kLeafThreads2)
     HEAD[p] = (p == 0 || !key_eq<KW>(K, cap, p, p - 1)) ? 1 : 0;
   __syncthreads();
-  const int ch = (n + kLeafThreads2 - 1) / kLeafThreads2;  // <= 8
+  const int ch = (n + kLeafThreads2 - 1) / kLeafThreads2;  // <= cap / threads <= 32
   const int p0 = tid * ch, p1 = min(n, p0 + ch);
   uint32_t keepbits = 0;
   for (int p = p0; p < p1; ++p) {
