@@ -79,6 +79,8 @@ struct Ctl {  // control arrays inside the workspace
   uint32_t* scan_total;   // 1: total merged terms
   double2* sums;          // [n] run sums, compacted per leaf
   uint32_t* rmap;         // emit range -> first leaf
+  u64* opk;               // [KW][ma (+ mb)] packed operand keys
+  uint8_t* opb;           // [ma (+ mb)] operand base phases
   u64* k1;               // [KW][n] item keys, buffer 1
   uint32_t* i1;          // [n]
   u64* k2;               // buffer 2
@@ -88,6 +90,7 @@ struct Ctl {  // control arrays inside the workspace
 struct Dims {
   int64_t n, ma, mb;     // items held here; |A|; B columns generated here
   int64_t n_space, j0;   // full raw-product size (sampling space); first B column
+  int64_t mb_all;        // |B| (all columns; packed operand keys cover A then all of B)
   int nb1, nsamp, leaf_cap, leaf_target, max_sub, max_leaves;
 };
 
@@ -423,12 +426,47 @@ k_sample(Layout L, Dims D, SrcA S, Ctl C) {
 }
 
 // ---------------------------------------------------- 2./4. count, scatter
-// Shared memory: splitters [KW][nb1] | hist nb1 | gbase nb1 | tile | (b, r) per item
+// Packing is a fixed bit permutation, so it commutes with XOR: the key of the
+// product a_i*b_j is pack(a_i) ^ pack(b_j).  k_pack_ops packs every operand
+// term once (and its base phase k + popc(x&z), sums.py:156-157); the item
+// generators then need KW XORs for the key and, per active word, the cross
+// phase 2popc(az&bx) - popc((ax^bx)&(az^bz)) (sums.py:134-136).
+template <int W, int KW, int MODE>
+__global__ void k_pack_ops(Layout L, SrcA S, int64_t ma, int64_t mb, Ctl C) {
+  const int64_t n = ma + (MODE == 0 ? mb : 0);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const bool isb = t >= ma;
+    const int64_t r = isb ? t - ma : t;
+    const u64* X = isb ? S.bx : S.ax;
+    const u64* Z = isb ? S.bz : S.az;
+    const uint8_t* K = isb ? S.bk : S.ak;
+    const int64_t ld = isb ? S.ldb : S.lda;
+    u64 zc[W], xc[W];
+    int base = K ? K[r] : 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const bool on = L.active >> w & 1;
+      xc[w] = on ? X[w * ld + r] : 0ull;
+      zc[w] = on ? Z[w * ld + r] : 0ull;
+      if (MODE == 0) base += popc64(xc[w] & zc[w]);
+    }
+    u64 key[KW];
+    pack_key<W, KW>(L, zc, xc, key);
+#pragma unroll
+    for (int d = 0; d < KW; ++d) C.opk[d * n + t] = key[d];
+    C.opb[t] = (uint8_t)(base & 3);
+  }
+}
+
+// Shared memory: splitters [KW][nb1] | hist nb1 | gbase nb1 | b tile | (b, r) per item
 struct GenSmem {
   u64* split;
   uint32_t* hist;
   uint32_t* gbase;
-  u64* tile;  // outer: [2W][kGenTB] b-term words (z then x)
+  u64* tile;       // outer: [2W][kGenTB] b-term words (z then x)
+  u64* tkey;       // outer: [KW][kGenTB] packed b-term keys
+  uint32_t* tpb;   // outer: [kGenTB] b-term base phases
   uint32_t* slot;  // per item: bucket << 16 | rank  (scatter only)
 };
 
@@ -439,8 +477,15 @@ __device__ __forceinline__ GenSmem gen_smem(u64* sm, int nb1, int KW) {
   g.hist = reinterpret_cast<uint32_t*>(sm + (int64_t)KW * nb1);
   g.gbase = g.hist + nb1;
   g.tile = reinterpret_cast<u64*>(g.gbase + nb1);  // 2*nb1 u32 keeps 8-byte alignment
-  g.slot = reinterpret_cast<uint32_t*>(g.tile + 2 * W * kGenTB);
+  g.tkey = g.tile + 2 * W * kGenTB;
+  g.tpb = reinterpret_cast<uint32_t*>(g.tkey + KW * kGenTB);
+  g.slot = g.tpb + kGenTB;
   return g;
+}
+
+__host__ __device__ constexpr size_t gen_smem_bytes(int W, int KW, int nb1) {
+  return (size_t)8 * KW * nb1 + 8 * (size_t)nb1 + (size_t)16 * W * kGenTB +
+         (size_t)8 * KW * kGenTB + 4 * (size_t)kGenTB + (size_t)4 * kGenTB * kGenThreads + 64;
 }
 
 template <int KW>
@@ -458,18 +503,19 @@ __device__ __forceinline__ void gen_prologue(const GenSmem& g, const Ctl& C, int
 // Sort: thread handles terms base + jj*blockDim + tid.
 template <int W, int KW, int MODE>
 struct Gen {
-  u64 ax[W], az[W];
-  int ka;
+  u64 ax[W], az[W], ka[KW];
+  int pa;
   int64_t i;
   bool valid_i;
 
   __device__ __forceinline__ void init(const Layout& L, const Dims& D, const SrcA& S,
-                                       const GenSmem& g) {
+                                       const Ctl& C, const GenSmem& g) {
     if (MODE == 0) {
       i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
       valid_i = i < D.ma;
+      const int64_t nops = D.ma + D.mb_all;
       const int64_t j0 = D.j0 + (int64_t)blockIdx.y * kGenTB;
-      // b tile into shared memory (z words then x words)
+      // b tile into shared memory: active z words then x words, packed keys, base phases
       for (int t = threadIdx.x; t < 2 * W * kGenTB; t += blockDim.x) {
         const int s = t / kGenTB, jj = t % kGenTB;
         const int w = s < W ? s : s - W;
@@ -479,55 +525,74 @@ struct Gen {
           v = s < W ? S.bz[w * S.ldb + j] : S.bx[w * S.ldb + j];
         g.tile[s * kGenTB + jj] = v;
       }
-      ka = 0;
+      for (int t = threadIdx.x; t < KW * kGenTB; t += blockDim.x) {
+        const int d = t / kGenTB, jj = t % kGenTB;
+        const int64_t j = j0 + jj;
+        g.tkey[t] = j < D.j0 + D.mb ? C.opk[d * nops + D.ma + j] : 0ull;
+      }
+      for (int jj = threadIdx.x; jj < kGenTB; jj += blockDim.x) {
+        const int64_t j = j0 + jj;
+        g.tpb[jj] = j < D.j0 + D.mb ? C.opb[D.ma + j] : 0u;
+      }
 #pragma unroll
       for (int w = 0; w < W; ++w) {
         const bool on = valid_i && (L.active >> w & 1);
         ax[w] = on ? S.ax[w * S.lda + i] : 0ull;
         az[w] = on ? S.az[w * S.lda + i] : 0ull;
       }
-      if (valid_i && S.ak) ka = S.ak[i];
+#pragma unroll
+      for (int d = 0; d < KW; ++d) ka[d] = valid_i ? C.opk[d * nops + i] : 0ull;
+      pa = valid_i ? C.opb[i] : 0;
     }
   }
 
   // item jj of this thread: returns false when out of range
-  __device__ __forceinline__ bool item(const Layout& L, const Dims& D, const SrcA& S,
+  __device__ __forceinline__ bool item(const Layout& L, const Dims& D, const Ctl& C,
                                        const GenSmem& g, int jj, u64 (&key)[KW], uint32_t& ik) {
-    u64 zc[W], xc[W];
     int64_t r;
     int k;
     if (MODE == 0) {
       const int64_t j = D.j0 + (int64_t)blockIdx.y * kGenTB + jj;  // global B index
       if (!valid_i || j >= D.j0 + D.mb) return false;
-      k = ka + (S.bk ? S.bk[j] : 0);
+      k = pa + (int)g.tpb[jj];
 #pragma unroll
       for (int w = 0; w < W; ++w) {
         if (L.active >> w & 1) {
           const u64 b_z = g.tile[w * kGenTB + jj], b_x = g.tile[(W + w) * kGenTB + jj];
-          k += phase_word(ax[w], az[w], b_x, b_z);
-          xc[w] = ax[w] ^ b_x;
-          zc[w] = az[w] ^ b_z;
-        } else {
-          xc[w] = zc[w] = 0;
+          k += 2 * popc64(az[w] & b_x) - popc64((ax[w] ^ b_x) & (az[w] ^ b_z));
         }
       }
+#pragma unroll
+      for (int d = 0; d < KW; ++d) key[d] = ka[d] ^ g.tkey[d * kGenTB + jj];
       r = j * D.ma + i;
     } else {
       r = (int64_t)blockIdx.x * blockDim.x * kGenTB + (int64_t)jj * blockDim.x + threadIdx.x;
       if (r >= D.n) return false;
-      k = S.ak ? S.ak[r] : 0;
+      k = C.opb[r];
 #pragma unroll
-      for (int w = 0; w < W; ++w) {
-        const bool on = L.active >> w & 1;
-        xc[w] = on ? S.ax[w * S.lda + r] : 0ull;
-        zc[w] = on ? S.az[w * S.lda + r] : 0ull;
-      }
+      for (int d = 0; d < KW; ++d) key[d] = C.opk[d * D.ma + r];
     }
-    pack_key<W, KW>(L, zc, xc, key);
     ik = ((uint32_t)r << 2) | (uint32_t)(k & 3);
     return true;
   }
 };
+
+// number of splitters <= key, branch-free with a fixed step count (all lanes
+// take the same path); top = largest power of two <= nsp (0 if nsp == 0)
+template <int KW>
+__device__ __forceinline__ int bucket_fixed(const u64 (&key)[KW], const u64* s, int64_t stride,
+                                            int nsp, int top) {
+  int pos = 0;
+  for (int step = top; step > 0; step >>= 1) {
+    const int c = pos + step;
+    if (c <= nsp && !key_lt<KW>(key, s, stride, c - 1)) pos = c;
+  }
+  return pos;
+}
+
+__device__ __forceinline__ int pow2_floor(int v) { return v > 0 ? 1 << (31 - __clz(v)) : 0; }
+
+constexpr int kGenIlp = 4;  // independent items per thread in flight
 
 template <int W, int KW, int MODE>
 __global__ void __launch_bounds__(kGenThreads)
@@ -536,16 +601,30 @@ k_count(Layout L, Dims D, SrcA S, Ctl C) {
   const GenSmem g = gen_smem<W>(sm, D.nb1, KW);
   gen_prologue<KW>(g, C, D.nb1);
   Gen<W, KW, MODE> gen;
-  gen.init(L, D, S, g);
+  gen.init(L, D, S, C, g);
   __syncthreads();
+  const int nsp = D.nb1 - 1, top = pow2_floor(nsp);
 #pragma unroll 1
-  for (int jj = 0; jj < kGenTB; ++jj) {
-    u64 key[KW];
-    uint32_t ik;
-    if (gen.item(L, D, S, g, jj, key, ik)) {
-      const int b = bucket_of<KW>(key, g.split, D.nb1, D.nb1 - 1);
-      atomicAdd(&g.hist[b], 1u);
+  for (int j0 = 0; j0 < kGenTB; j0 += kGenIlp) {
+    u64 key[kGenIlp][KW];
+    bool ok[kGenIlp];
+    int pos[kGenIlp];
+#pragma unroll
+    for (int u = 0; u < kGenIlp; ++u) {
+      uint32_t ik;
+      ok[u] = gen.item(L, D, C, g, j0 + u, key[u], ik);
+      pos[u] = 0;
     }
+    for (int step = top; step > 0; step >>= 1) {
+#pragma unroll
+      for (int u = 0; u < kGenIlp; ++u) {
+        const int c = pos[u] + step;
+        if (c <= nsp && !key_lt<KW>(key[u], g.split, D.nb1, c - 1)) pos[u] = c;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kGenIlp; ++u)
+      if (ok[u]) atomicAdd(&g.hist[pos[u]], 1u);
   }
   __syncthreads();
   for (int b = threadIdx.x; b < D.nb1; b += blockDim.x)
@@ -559,31 +638,45 @@ k_scatter(Layout L, Dims D, SrcA S, Ctl C) {
   const GenSmem g = gen_smem<W>(sm, D.nb1, KW);
   gen_prologue<KW>(g, C, D.nb1);
   Gen<W, KW, MODE> gen;
-  gen.init(L, D, S, g);
+  gen.init(L, D, S, C, g);
   __syncthreads();
+  const int nsp = D.nb1 - 1, top = pow2_floor(nsp);
 #pragma unroll 1
-  for (int jj = 0; jj < kGenTB; ++jj) {
-    u64 key[KW];
-    uint32_t ik;
-    uint32_t code = 0xFFFFFFFFu;
-    if (gen.item(L, D, S, g, jj, key, ik)) {
-      const int b = bucket_of<KW>(key, g.split, D.nb1, D.nb1 - 1);
-      const uint32_t rk = atomicAdd(&g.hist[b], 1u);
-      code = ((uint32_t)b << 16) | rk;
+  for (int j0 = 0; j0 < kGenTB; j0 += kGenIlp) {
+    u64 key[kGenIlp][KW];
+    bool ok[kGenIlp];
+    int pos[kGenIlp];
+#pragma unroll
+    for (int u = 0; u < kGenIlp; ++u) {
+      uint32_t ik;
+      ok[u] = gen.item(L, D, C, g, j0 + u, key[u], ik);
+      pos[u] = 0;
     }
-    g.slot[jj * kGenThreads + threadIdx.x] = code;
+    for (int step = top; step > 0; step >>= 1) {
+#pragma unroll
+      for (int u = 0; u < kGenIlp; ++u) {
+        const int c = pos[u] + step;
+        if (c <= nsp && !key_lt<KW>(key[u], g.split, D.nb1, c - 1)) pos[u] = c;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kGenIlp; ++u) {
+      uint32_t code = 0xFFFFFFFFu;
+      if (ok[u]) code = ((uint32_t)pos[u] << 16) | atomicAdd(&g.hist[pos[u]], 1u);
+      g.slot[(j0 + u) * kGenThreads + threadIdx.x] = code;
+    }
   }
   __syncthreads();
   for (int b = threadIdx.x; b < D.nb1; b += blockDim.x)
     if (g.hist[b]) g.gbase[b] = atomicAdd(&C.bcursor[b], g.hist[b]);
   __syncthreads();
-#pragma unroll 1
+#pragma unroll 4
   for (int jj = 0; jj < kGenTB; ++jj) {
     const uint32_t code = g.slot[jj * kGenThreads + threadIdx.x];
     if (code == 0xFFFFFFFFu) continue;
     u64 key[KW];
     uint32_t ik;
-    gen.item(L, D, S, g, jj, key, ik);
+    gen.item(L, D, C, g, jj, key, ik);
     const uint32_t pos = g.gbase[code >> 16] + (code & 0xFFFFu);
     store_key<KW>(C.k1, D.n, pos, key);
     C.i1[pos] = ik;
@@ -881,7 +974,7 @@ static inline int64_t align256(int64_t v) { return (v + 255) & ~(int64_t)255; }
 
 struct WsLayout {
   int64_t split, bcount, bbase, bcursor, leaf_off, n_leaves, leaf_ctr, tile_off, n_tiles,
-      sub_count, leaf_desc, split2, kept, kprefix, scan, k1, i1, k2, i2, sums, rmap, total;
+      sub_count, leaf_desc, split2, kept, kprefix, scan, k1, i1, k2, i2, sums, rmap, opk, opb, total;
 };
 
 static WsLayout ws_layout(const pl_merge_plan& P) {
@@ -911,6 +1004,8 @@ static WsLayout ws_layout(const pl_merge_plan& P) {
   w.i2 = o; o = align256(o + 4 * n);
   w.sums = o; o = align256(o + 16 * n);
   w.rmap = o; o = align256(o + 4 * (n / 128 + 2));
+  w.opk = o; o = align256(o + 8 * KW * (P.ma + P.mb));
+  w.opb = o; o = align256(o + (P.ma + P.mb));
   w.total = o;
   (void)ctl_end;
   return w;
@@ -1054,6 +1149,7 @@ static Dims to_dims(const pl_merge_plan& P) {
   D.mb = P.mb;
   D.n_space = P.n_items;
   D.j0 = 0;
+  D.mb_all = P.mb;
   D.nb1 = P.n_buckets;
   D.nsamp = P.n_samples;
   D.leaf_cap = P.leaf_cap;
@@ -1085,6 +1181,8 @@ static Ctl to_ctl(const pl_merge_plan& P, void* ws) {
   C.scan_total = C.scan_scratch + scan_scratch_words(P.n_buckets * (int64_t)P.max_sub);
   C.sums = (double2*)(b + w.sums);
   C.rmap = (uint32_t*)(b + w.rmap);
+  C.opk = (u64*)(b + w.opk);
+  C.opb = (uint8_t*)(b + w.opb);
   C.k1 = (u64*)(b + w.k1);
   C.i1 = (uint32_t*)(b + w.i1);
   C.k2 = (u64*)(b + w.k2);
@@ -1102,6 +1200,13 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const O
   const WsLayout wl = ws_layout(P);
   PLB_CUDA(cudaMemsetAsync(ws, 0, (size_t)wl.leaf_desc, st));  // control region
 
+  {
+    StageTimer t_(st, "k_pack_ops");
+    const int64_t nops = D.ma + (MODE == 0 ? D.mb_all : 0);
+    k_pack_ops<W, KW, MODE><<<(unsigned)std::min<int64_t>(ceil_div(nops, 256), 8 * num_sms()), 256,
+                              0, st>>>(L, S, D.ma, D.mb_all, C);
+    PLB_CHECK_LAUNCH("k_pack_ops");
+  }
   // 1-2. splitters + counts
   if (D.nb1 > 1) {
     const size_t sm1 = (size_t)D.nsamp * (8 * KW + 4) + 16;
@@ -1110,8 +1215,7 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const O
     k_sample<W, KW, MODE><<<1, kLeafThreads, sm1, st>>>(L, D, S, C);
     PLB_CHECK_LAUNCH("k_sample");
   }
-  const size_t gsm = (size_t)8 * KW * D.nb1 + 8 * D.nb1 + 8 + (size_t)16 * W * kGenTB +
-                     (size_t)4 * kGenTB * kGenThreads + 64;
+  const size_t gsm = gen_smem_bytes(W, KW, D.nb1);
   dim3 ggrid;
   if (MODE == 0) ggrid = dim3((unsigned)ceil_div(D.ma, kGenThreads), (unsigned)ceil_div(D.mb, kGenTB));
   else ggrid = dim3((unsigned)ceil_div(D.n, (int64_t)kGenThreads * kGenTB), 1);
@@ -1228,6 +1332,13 @@ static int run_partition(const pl_merge_plan& P, const SrcA& S, int64_t j0, int6
   const WsLayout wl = ws_layout(Q);
   PLB_CUDA(cudaMemsetAsync(ws, 0, (size_t)wl.leaf_desc, st));
   if (D.n > 0) {
+    {
+      StageTimer t_(st, "k_pack_ops");
+      const int64_t nops = D.ma + D.mb_all;
+      k_pack_ops<W, KW, 0><<<(unsigned)std::min<int64_t>(ceil_div(nops, 256), 8 * num_sms()), 256,
+                             0, st>>>(L, S, D.ma, D.mb_all, C);
+      PLB_CHECK_LAUNCH("k_pack_ops");
+    }
     if (D.nb1 > 1) {
       const size_t sm1 = (size_t)D.nsamp * (8 * KW + 4) + 16;
       if (set_smem(k_sample<W, KW, 0>, sm1)) return PL_ERR_CUDA;
@@ -1235,8 +1346,7 @@ static int run_partition(const pl_merge_plan& P, const SrcA& S, int64_t j0, int6
       k_sample<W, KW, 0><<<1, kLeafThreads, sm1, st>>>(L, D, S, C);
       PLB_CHECK_LAUNCH("k_sample");
     }
-    const size_t gsm = (size_t)8 * KW * D.nb1 + 8 * D.nb1 + 8 + (size_t)16 * W * kGenTB +
-                       (size_t)4 * kGenTB * kGenThreads + 64;
+    const size_t gsm = gen_smem_bytes(W, KW, D.nb1);
     const dim3 ggrid((unsigned)ceil_div(D.ma, kGenThreads), (unsigned)ceil_div(D.mb, kGenTB));
     if (D.nb1 > 1) {
       if (set_smem(k_count<W, KW, 0>, gsm)) return PL_ERR_CUDA;

@@ -15,10 +15,10 @@
 // which no splitter can divide) are sorted in place in global memory.
 #pragma once
 
-// Shared-memory items per leaf buffer for key width KW (two buffers of about
-// 23 KB per CTA so four CTAs fit on one SM).
+// Shared-memory items per leaf for key width KW (a multiple of the CTA size;
+// about 32 KB of shared memory per CTA with the radix scratch -> 7 CTAs/SM).
 __host__ __device__ constexpr int leaf_cap_for(int KW) {
-  return KW <= 2 ? 512 : KW == 4 ? 256 : KW == 8 ? 128 : KW == 16 ? 64 : 32;
+  return KW <= 2 ? 768 : KW == 4 ? 384 : KW == 8 ? 256 : 128;
 }
 
 __host__ __device__ constexpr size_t leaf_buf_stride(int KW) {
@@ -229,6 +229,7 @@ __device__ __forceinline__ uint32_t key_window(const u64* K, int stride, int t, 
 
 template <int KW, int CAP>
 __device__ __noinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint8_t* scratch) {
+  static_assert(CAP % kLeafThreads2 == 0, "leaf capacity must be a multiple of the CTA size");
   constexpr int SEG = CAP / kLeafWarps2;             // max positions owned by one warp
   constexpr int SLOTS = SEG >= 32 ? SEG / 32 : 1;
   // only the first npos positions take part: warps own seg = npos / 8 each
@@ -532,8 +533,13 @@ k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
   if (tid == 0) C.kept[leaf] = kept;
 }
 
+// leaf buffer + scratch (radix sort, then the run sums SUM[cap])
 __host__ __device__ constexpr size_t leaf_sort_smem_bytes(int KW) {
-  return leaf_buf_stride(KW) + radix_smem_bytes(leaf_cap_for(KW)) + 64;
+  return leaf_buf_stride(KW) +
+         (radix_smem_bytes(leaf_cap_for(KW)) > 16 * (size_t)leaf_cap_for(KW)
+              ? radix_smem_bytes(leaf_cap_for(KW))
+              : 16 * (size_t)leaf_cap_for(KW)) +
+         64;
 }
 
 // ------------------------------------------------------------ emit
