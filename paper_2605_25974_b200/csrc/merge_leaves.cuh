@@ -461,7 +461,14 @@ __device__ __noinline__ uint32_t leaf_sort_global(const Dims& D, const SrcA& S, 
   return base;
 }
 
-constexpr int kSortCtasPerSm = 8;
+// runs of two or more items (kept out of line: rare in most workloads)
+template <int W, int KW, int MODE>
+__device__ __noinline__ double2 run_sum_multi(const SrcA& S, int64_t ma, const uint32_t* I,
+                                              int p, int m) {
+  return RunSum<W, KW, MODE>::run(S, ma, I, p, m);
+}
+
+constexpr int kSortCtasPerSm = 7;  // bounded by shared memory (~32 KB per CTA)
 
 template <int W, int KW, int MODE>
 __global__ void __launch_bounds__(kLeafThreads2, kSortCtasPerSm)
@@ -471,12 +478,11 @@ k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
   __shared__ uint32_t s_warp[kLeafWarps2];
   const int tid = threadIdx.x;
   const uint32_t leaf = blockIdx.x;
+  const uint4 dsc = C.leaf_desc[leaf];  // (in bounds: grid = max_leaves) issued with n_leaves
   if (leaf >= *C.n_leaves) {
     if (tid == 0) C.kept[leaf] = 0;
     return;
   }
-  using RS = RunSum<W, KW, MODE>;
-  const uint4 dsc = C.leaf_desc[leaf];
   const int n = (int)dsc.z;
   const uint32_t off = dsc.y;
   const u64* GK = (dsc.x == 1 ? C.k1 : C.k2) + off;
@@ -507,16 +513,32 @@ k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
   for (int p = tid; p < n; p += kLeafThreads2)
     HEAD[p] = (p == 0 || !key_eq<KW>(K, cap, p, p - 1)) ? 1 : 0;
   __syncthreads();
-  const int ch = (n + kLeafThreads2 - 1) / kLeafThreads2;  // <= cap / threads <= 32
+  constexpr int CH = cap / kLeafThreads2;  // max items per thread
+  const int ch = (n + kLeafThreads2 - 1) / kLeafThreads2;
   const int p0 = tid * ch, p1 = min(n, p0 + ch);
+  // coefficients of the chunk's items, all gathers in flight together; a run
+  // of one item is its coefficient (RunSum::run with m == 1), longer runs
+  // are summed by RunSum in numpy's order
+  double2 cf[CH];
+  uint8_t hd[CH];
+#pragma unroll
+  for (int u = 0; u < CH; ++u) {
+    hd[u] = 0;
+    if (u < ch && p0 + u < p1) {
+      hd[u] = HEAD[p0 + u];
+      cf[u] = Source<W, KW, MODE>::coef(S, D.ma, I[p0 + u]);
+    }
+  }
   uint32_t keepbits = 0;
-  for (int p = p0; p < p1; ++p) {
-    if (!HEAD[p]) continue;
+#pragma unroll
+  for (int u = 0; u < CH; ++u) {
+    const int p = p0 + u;
+    if (u >= ch || p >= p1 || !hd[u]) continue;
     int q = p + 1;
     while (q < n && !HEAD[q]) ++q;
-    const double2 s = RS::run(S, D.ma, I, p, q - p);
+    const double2 s = q == p + 1 ? cf[u] : run_sum_multi<W, KW, MODE>(S, D.ma, I, p, q - p);
     if (keep_sum(s, eps)) {
-      keepbits |= 1u << (p - p0);
+      keepbits |= 1u << u;
       SUM[p] = s;
     }
   }
