@@ -258,24 +258,47 @@ def main():
         tot_ms = float(t.item())
     value = n_items * args.steps / (tot_ms / 1e3)
 
-    # dominant kernel roofline (k_leaves: read items, write merged records)
+    # roofline per pipeline kernel (algorithmic bytes per launch),
+    # reported for the dominant one (largest share of the step)
     plan = pl.sums.LAST_PLAN or {}
     kw = plan.get("key_words", 2)
-    leaf_ms = [ms for nm, ms in stages if nm == "k_leaves"]
     hbm, peak_kind = measured_peaks()
+    local_items = plan.get("n_items", n_items)
+    local_out = counts[-1]
+    item_b = 8 * kw + 4                       # packed key + ik
+    ent_b = 8 * kw + 16                       # merged (key, sum) entry
+    term_b = 16 * 8 + 1 + 16                  # SoA output term at W=8
+    algo = {
+        "k_scatter": (local_items * item_b, f"{item_b} B item written"),
+        "k_split": (3 * local_items * item_b,
+                    f"{item_b} B item read twice (classify, move) + written once"),
+        "k_leaf_sort": (local_items * item_b + local_out * ent_b,
+                        f"{item_b} B item read + {ent_b} B (key, sum) per merged term written"),
+        "k_emit": (local_out * (ent_b + term_b),
+                   f"{ent_b} B (key, sum) read + {term_b} B SoA term written per merged term"),
+    }
+    per_kernel = {}
+    for nm, (bts, desc) in algo.items():
+        ms = [m for k2, m in stages if k2 == nm]
+        if not ms:
+            continue
+        avg = statistics.mean(ms) / 1e3
+        ach = bts / avg / 1e9
+        per_kernel[nm] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                          "frac": ach / hbm, "avg_launch_ms": avg * 1e3,
+                          "algorithmic_bytes_per_launch": bts, "bytes_per_unit": desc,
+                          "traffic": ncu_traffic(nm)}
     roofline = None
-    if leaf_ms:
-        local_items = plan.get("n_items", n_items)
-        local_out = counts[-1]
-        algo = local_items * (8 * kw + 4) + local_out * (16 * 8 + 1 + 16)
-        avg = statistics.mean(leaf_ms) / 1e3
-        achieved = algo / avg / 1e9
-        roofline = {"kernel": "k_leaves", "bound": "hbm", "achieved": achieved, "peak": hbm,
-                    "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic("k_leaves"),
-                    "peak_source": peak_kind,
-                    "algorithmic_bytes_per_launch": algo,
-                    "bytes_per_unit": f"{8 * kw + 4} B item read + {16 * 8 + 17} B per merged term",
-                    "avg_launch_ms": avg * 1e3}
+    if per_kernel:
+        dom = max(per_kernel, key=lambda k2: per_kernel[k2]["avg_launch_ms"])
+        roofline = dict(per_kernel[dom], kernel=dom, peak_source=peak_kind)
+        step_bytes = local_out * term_b + sum_bytes(A) + sum_bytes(B)
+        step_s = (tot_ms / args.steps) / 1e3
+        roofline["step"] = {"algorithmic_bytes": step_bytes,
+                            "bytes_per_unit": f"{term_b} B output term + operands read",
+                            "achieved": step_bytes / step_s / 1e9,
+                            "frac": step_bytes / step_s / 1e9 / hbm}
+        roofline["kernels"] = per_kernel
     stage_share = {}
     for nm, ms in stages:
         stage_share[nm] = stage_share.get(nm, 0.0) + ms

@@ -977,10 +977,19 @@ struct WsLayout {
       sub_count, leaf_desc, split2, kept, kprefix, scan, k1, i1, k2, i2, sums, rmap, opk, opb, total;
 };
 
+// Bound on the number of leaves: a bucket of s items gets at most
+// ceil(s / leaf_target) leaves, so the total is <= n / leaf_target + nb1.
+static inline int64_t plan_max_leaves(const pl_merge_plan& P) {
+  const int64_t by_sub = (int64_t)P.n_buckets * P.max_sub;
+  const int64_t by_size = P.n_items / std::max(1, P.leaf_target) + P.n_buckets + 1;
+  return std::min(by_sub, by_size);
+}
+
 static WsLayout ws_layout(const pl_merge_plan& P) {
   WsLayout w{};
   const int64_t KW = P.key_words, nb1 = P.n_buckets, n = P.n_items;
-  const int64_t max_leaves = nb1 * (int64_t)P.max_sub;
+  const int64_t sub_slots = nb1 * (int64_t)P.max_sub;  // [bucket][sub] tables
+  const int64_t max_leaves = plan_max_leaves(P);
   int64_t o = 0;
   w.split = o; o = align256(o + 8 * KW * nb1);
   w.bcount = o; o = align256(o + 4 * nb1);
@@ -991,10 +1000,10 @@ static WsLayout ws_layout(const pl_merge_plan& P) {
   w.leaf_ctr = o; o = align256(o + 4);
   w.tile_off = o; o = align256(o + 4 * (nb1 + 1));
   w.n_tiles = o; o = align256(o + 4);
-  w.sub_count = o; o = align256(o + 4 * max_leaves);
+  w.sub_count = o; o = align256(o + 4 * sub_slots);
   const int64_t ctl_end = o;  // everything above is zeroed per call
   w.leaf_desc = o; o = align256(o + 16 * max_leaves);
-  w.split2 = o; o = align256(o + 8 * KW * max_leaves);
+  w.split2 = o; o = align256(o + 8 * KW * sub_slots);
   w.kept = o; o = align256(o + 4 * max_leaves);
   w.kprefix = o; o = align256(o + 4 * max_leaves);
   w.scan = o; o = align256(o + 4 * (scan_scratch_words(max_leaves) + 1));
@@ -1155,7 +1164,7 @@ static Dims to_dims(const pl_merge_plan& P) {
   D.leaf_cap = P.leaf_cap;
   D.leaf_target = P.leaf_target;
   D.max_sub = P.max_sub;
-  D.max_leaves = P.n_buckets * P.max_sub;
+  D.max_leaves = (int)plan_max_leaves(P);
   return D;
 }
 
@@ -1178,7 +1187,7 @@ static Ctl to_ctl(const pl_merge_plan& P, void* ws) {
   C.kept = (uint32_t*)(b + w.kept);
   C.kprefix = (uint32_t*)(b + w.kprefix);
   C.scan_scratch = (uint32_t*)(b + w.scan);
-  C.scan_total = C.scan_scratch + scan_scratch_words(P.n_buckets * (int64_t)P.max_sub);
+  C.scan_total = C.scan_scratch + scan_scratch_words(plan_max_leaves(P));
   C.sums = (double2*)(b + w.sums);
   C.rmap = (uint32_t*)(b + w.rmap);
   C.opk = (u64*)(b + w.opk);
