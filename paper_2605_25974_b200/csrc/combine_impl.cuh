@@ -49,7 +49,9 @@ constexpr int kGenTB = 16;        // b-terms per tile (outer) / terms per thread
 constexpr int kLeafThreads = 512;
 constexpr int kSplitThreads = 512;
 constexpr int kSortSmemBytes = 200 * 1024;
-constexpr int kSampleOversample = 16;
+constexpr int kSampleOversample = 16;  // level-2 samples per sub-bucket
+constexpr int kSample1Oversample = 16;  // level-1 samples per bucket
+constexpr int kLeavesPerBucket = 32;
 constexpr int kMaxBuckets = 2048;
 constexpr int kSplitTile = 4096;     // items per level-2 classification tile
 constexpr int kSplitTileThreads = 256;
@@ -1051,13 +1053,15 @@ static void finish_plan(pl_merge_plan* P, const u64* masks /* z[W] then x[W] */)
   const int64_t n = P->n_items;
   int64_t nb1 = 1;
   if (n > cap) {
-    nb1 = (n + P->leaf_target - 1) / P->leaf_target;
-    const int64_t nb_max = std::min<int64_t>(kMaxBuckets, scap / kSampleOversample);
+    // level 1 aims at ~kLeavesPerBucket leaves per bucket (fewer, cheaper
+    // samples for small inputs); level 2 adapts to the exact bucket sizes
+    nb1 = ceil_div(n, (int64_t)kLeavesPerBucket * P->leaf_target);
+    const int64_t nb_max = std::min<int64_t>(kMaxBuckets, scap / kSample1Oversample);
     if (nb1 > nb_max) nb1 = nb_max;
     if (nb1 < 2) nb1 = 2;
   }
   P->n_buckets = (int)nb1;
-  P->n_samples = nb1 > 1 ? (int)std::min<int64_t>(n, std::min<int64_t>(scap, nb1 * kSampleOversample)) : 0;
+  P->n_samples = nb1 > 1 ? (int)std::min<int64_t>(n, std::min<int64_t>(scap, nb1 * kSample1Oversample)) : 0;
   // level-2 sample capacity bounds the sub-bucket count
   // level-2 sample (one CTA, <= 160 KB): >= 8 samples per sub-bucket
   const int s2cap = std::max(64, std::min(8192, (160 * 1024) / (8 * KW + 4)));

@@ -3,7 +3,8 @@ sys.path.insert(0, '.')
 import paper_2605_25974_b200 as pl
 from paper_2605_25974_b200 import rng, _native
 dev = torch.device('cuda', 0)
-a, b = rng.config_columns(4)
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+a, b = rng.config_columns(cfg)
 A = pl.PauliSumSoA.from_columns(500, *a, device=dev)
 B = pl.PauliSumSoA.from_columns(500, *b, device=dev)
 for it in range(6):
