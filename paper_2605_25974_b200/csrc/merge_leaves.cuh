@@ -478,6 +478,13 @@ k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
   __shared__ uint32_t s_warp[kLeafWarps2];
   const int tid = threadIdx.x;
   const uint32_t leaf = blockIdx.x;
+#ifdef PLB_LEAF_PROF
+  long long tp[8];
+  tp[0] = clock64();
+#define LEAF_T(i) tp[i] = clock64()
+#else
+#define LEAF_T(i)
+#endif
   const uint4 dsc = C.leaf_desc[leaf];  // (in bounds: grid = max_leaves) issued with n_leaves
   if (leaf >= *C.n_leaves) {
     if (tid == 0) C.kept[leaf] = 0;
@@ -509,10 +516,13 @@ k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
     I[t] = GI[t];
   }
   __syncthreads();
+  LEAF_T(1);
   if (n > 1 && !radix_sort_leaf<KW, cap>(K, I, n, scratch)) bitonic_sort_local<KW, cap>(K, I, n);
+  LEAF_T(2);
   for (int p = tid; p < n; p += kLeafThreads2)
     HEAD[p] = (p == 0 || !key_eq<KW>(K, cap, p, p - 1)) ? 1 : 0;
   __syncthreads();
+  LEAF_T(3);
   constexpr int CH = cap / kLeafThreads2;  // max items per thread
   const int ch = (n + kLeafThreads2 - 1) / kLeafThreads2;
   const int p0 = tid * ch, p1 = min(n, p0 + ch);
@@ -542,10 +552,12 @@ k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
       SUM[p] = s;
     }
   }
+  LEAF_T(4);
   uint32_t kept;
   uint32_t slot = leaf_excl_scan(__popc(keepbits), s_warp, &kept);
   for (uint32_t bb = keepbits; bb; bb &= bb - 1) POS[slot++] = (uint16_t)(p0 + __ffs(bb) - 1);
   __syncthreads();
+  LEAF_T(5);
   for (uint32_t q = tid; q < kept; q += kLeafThreads2) {
     const int p = POS[q];
 #pragma unroll
@@ -553,6 +565,12 @@ k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
     DS[q] = SUM[p];
   }
   if (tid == 0) C.kept[leaf] = kept;
+#ifdef PLB_LEAF_PROF
+  LEAF_T(6);
+  if (tid == 0 && (leaf % 20011) == 5)
+    printf("LEAFPROF n=%d load=%lld sort=%lld head=%lld sums=%lld scan=%lld write=%lld\n", n,
+           tp[1] - tp[0], tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], tp[6] - tp[5]);
+#endif
 }
 
 // leaf buffer + scratch (radix sort, then the run sums SUM[cap])
