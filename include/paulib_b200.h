@@ -207,6 +207,34 @@ int pl_group_greedy(int W, int64_t M, const uint64_t* x, const uint64_t* z, int6
                     void* workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------
+ * §8(f) f2 — Clifford conjugation in place.  Replaces gates.py:72-102
+ * (apply_clifford_inplace, called by _SumBase.apply_clifford, sums.py:309-316):
+ * every term P becomes U P U^dagger for gate H (0), S (1), CNOT (2, q0 =
+ * control, q1 = target) or CZ (3); x, z, k are device SoA planes / phases,
+ * modified in place.  Qubit indices must be < 64*W (the Python layer checks
+ * them against n and raises IndexError as the reference does, gates.py:23-24).
+ */
+int pl_apply_clifford(int W, int64_t M, uint64_t* x, uint64_t* z, uint8_t* k, int64_t ld,
+                      int gate, int q0, int q1, void* stream);
+
+/* ------------------------------------------------------------------------
+ * §8(f) f1 — Pauli-rotation split, un-combined.  Replaces _rotation_columns
+ * (sums.py:177-223).  gen_x / gen_z are HOST arrays of W words (the phase-free
+ * generator P); cos_t is the snapped cosine (rotations.py:24-35) and
+ * (msin_re, msin_im) the complex factor -1j*sin_t as the reference's Python
+ * evaluates it.  Output: M terms (sin == 0 or cos == 0) or M + #anti
+ * interleaved terms; ldo >= 2*M in the split case.  *out_count (device) gets
+ * the output term count.  Apply pl_sort_combine afterwards for the canonical
+ * form (apply_rotation, sums.py:318-325).
+ */
+int64_t pl_rotation_workspace_bytes(int64_t M);
+int pl_rotation_split(int W, int64_t M, const uint64_t* x, const uint64_t* z, const uint8_t* k,
+                      const double* c, int64_t ld, const uint64_t* gen_x, const uint64_t* gen_z,
+                      double cos_t, double msin_re, double msin_im, void* workspace,
+                      size_t workspace_bytes, uint64_t* ox, uint64_t* oz, uint8_t* ok, double* oc,
+                      int64_t ldo, int64_t* out_count, void* stream);
+
+/* ------------------------------------------------------------------------
  * Stage timing (instrumentation for bench.py).  While enabled, multi-kernel
  * entry points record a CUDA event pair around every kernel they launch, on
  * the launching stream.  pl_stage_times() waits for the recorded events and

@@ -170,3 +170,75 @@ def pack_bitrows(bits: np.ndarray) -> np.ndarray:
     pad = np.zeros((r, nw * 32), np.uint8)
     pad[:, :c] = bits
     return np.packbits(pad, axis=1, bitorder="little").view("<u4").astype(np.uint32).reshape(r, nw)
+
+
+# ---------------------------------------------------------------- §8(f) f1/f2
+def apply_clifford(x, z, flags, gate: str, qubits, n: int):
+    """U P U^dagger over every row (gates.py:31-102), returned as copies.
+    H: swap the x/z bits, sign flip where the letter is Y; S: z ^= x, flip
+    where Y; CNOT(c,t): x_t ^= x_c, z_c ^= z_t, flip where x_c z_t (x_t ^ z_c ^ 1);
+    CZ(c,t): z_c ^= x_t, z_t ^= x_c, flip where x_c x_t (z_c ^ z_t)."""
+    x, z, f = x.copy(), z.copy(), flags.copy()
+    one = np.uint64(1)
+
+    def bit(a, q):
+        return (a[:, q // 64] >> np.uint64(q % 64)) & one
+
+    gate = gate.upper()
+    if gate in ("H", "S"):
+        (q,) = qubits
+        w, m = q // 64, np.uint64(1 << (q % 64))
+        xb, zb = x[:, w] & m, z[:, w] & m
+        if gate == "H":
+            f ^= (((xb & zb) != 0).astype(np.uint8) << 1)
+            x[:, w] = (x[:, w] & ~m) | zb
+            z[:, w] = (z[:, w] & ~m) | xb
+        else:
+            f ^= (((xb & z[:, w]) != 0).astype(np.uint8) << 1)
+            z[:, w] ^= xb
+        return x, z, f
+    c, t = qubits
+    xc, zc, xt, zt = bit(x, c), bit(z, c), bit(x, t), bit(z, t)
+    if gate == "CNOT":
+        cond = xc & zt & (xt ^ zc ^ one)
+        x[:, t // 64] ^= xc << np.uint64(t % 64)
+        z[:, c // 64] ^= zt << np.uint64(c % 64)
+    else:
+        cond = xc & xt & (zc ^ zt)
+        z[:, c // 64] ^= xt << np.uint64(c % 64)
+        z[:, t // 64] ^= xc << np.uint64(t % 64)
+    f ^= (cond.astype(np.uint8) << 1)
+    return x, z, f
+
+
+def rotation_split(x, z, flags, coeffs, gx, gz, cos_t: float, sin_t: float):
+    """Un-combined rotation split (sums.py:177-223): commuting rows pass,
+    an anti-commuting row becomes (c*cos, Q) then (c*(-1j*sin)*i^k, P*Q
+    letters, flags 0), k = flags + phase(P, Q); sin == 0 scales, cos == 0
+    replaces in place."""
+    gxm = np.broadcast_to(gx, x.shape)
+    gzm = np.broadcast_to(gz, z.shape)
+    anti = sip(x, z, gxm, gzm).astype(bool)
+    m, words = x.shape
+    if sin_t == 0.0:
+        return x.copy(), z.copy(), flags.copy(), np.where(anti, coeffs * cos_t, coeffs)
+    pk = (flags[anti].astype(np.int64) + phase_exponent(gxm[anti], gzm[anti], x[anti], z[anti])) % 4
+    prod = coeffs[anti] * (-1j * sin_t) * _PHASE[pk]
+    if cos_t == 0.0:
+        ox, oz, of, oc = x.copy(), z.copy(), flags.copy(), coeffs.copy()
+        ox[anti] ^= gx
+        oz[anti] ^= gz
+        of[anti] = 0
+        oc[anti] = prod
+        return ox, oz, of, oc
+    total = m + int(anti.sum())
+    first = np.cumsum(np.concatenate(([0], 1 + anti.astype(np.int64))))[:m]
+    second = first[anti] + 1
+    ox = np.empty((total, words), np.uint64)
+    oz = np.empty((total, words), np.uint64)
+    of = np.empty(total, np.uint8)
+    oc = np.empty(total, np.complex128)
+    ox[first], oz[first], of[first] = x, z, flags
+    oc[first] = np.where(anti, coeffs * cos_t, coeffs)
+    ox[second], oz[second], of[second], oc[second] = x[anti] ^ gx, z[anti] ^ gz, 0, prod
+    return ox, oz, of, oc

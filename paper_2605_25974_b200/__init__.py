@@ -17,6 +17,7 @@ from .sums import (PauliSum, PauliSumSoA, PauliTerm, outer_multiply, sort_and_co
 from .grouping import (CommutationPartition, GroupingStats, ValidationReport, group_assignment,
                        group_greedy, validate_partition)
 from .bitmatrix import commutation_bitmatrix, unpack_bits
+from .rotations import RotationSpec, TRIG_SNAP, reorder_rotation, trig_values
 from .rng import SplitMix64, config_columns, random_columns, random_sum
 from ._native import NativeLibraryError
 
@@ -33,6 +34,7 @@ __all__ = [
     "CommutationPartition", "GroupingStats", "ValidationReport", "group_assignment",
     "group_greedy", "validate_partition",
     "commutation_bitmatrix", "unpack_bits",
+    "RotationSpec", "TRIG_SNAP", "reorder_rotation", "trig_values",
     "SplitMix64", "config_columns", "random_columns", "random_sum",
     "NativeLibraryError", "__version__",
 ]

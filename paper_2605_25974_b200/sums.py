@@ -271,6 +271,42 @@ class PauliSumSoA:
             raise ValueError("eps must be >= 0")
         return sort_combine(self, eps=eps)
 
+    def apply_clifford(self, gate: str, qubits) -> None:
+        """Conjugate every term in place; term count unchanged (sums.py:309-316)."""
+        from . import gates
+
+        qubits = (int(qubits),) if isinstance(qubits, (int, np.integer)) else tuple(
+            int(q) for q in qubits)
+        code, q0, q1 = gates.check_gate(gate, qubits, self.n)
+        dev, back = _compute_device(self)
+        if len(self) == 0:
+            return
+        S = self.to(dev).planes()
+        gates.apply_clifford_planes(S.x, S.z, S.k, S.ld, S.W, S.M, code, q0, q1, dev)
+        if back or S.x.data_ptr() != self.x.data_ptr() or S.k.data_ptr() != self.flags.data_ptr():
+            self.x.copy_(S.x)
+            self.z.copy_(S.z)
+            self.flags.copy_(S.k)
+
+    def apply_rotation(self, rot, *, eps: float = 0.0, combine: bool = True):
+        """Conjugate by exp(-i*theta/2 * P): at most 2x the terms, canonical
+        unless combine=False (sums.py:318-325)."""
+        from .rotations import check_rotation_n, rotation_split
+
+        check_rotation_n(self.n, rot)
+        if eps < 0:
+            raise ValueError("eps must be >= 0")
+        dev, back = _compute_device(self)
+        with torch.cuda.device(dev):
+            if len(self) == 0:
+                out = PauliSumSoA.empty(self.n, device=dev)
+            else:
+                x, z, k, c = rotation_split(self.to(dev).planes(), rot, dev)
+                out = _new_sum(self.n, x, z, k, c)
+        if combine:
+            out = sort_combine(out, eps=eps)
+        return _download(out) if back else out
+
     def truncate(self, eps: float):
         """Drop terms with |coeff| <= eps, keeping order (sums.py:327-339)."""
         if eps < 0:
@@ -396,6 +432,19 @@ class PauliSum:
         if eps < 0:
             raise ValueError("eps must be >= 0")
         return self.to_soa().sort_and_combine(eps).to_aos()
+
+    def apply_clifford(self, gate: str, qubits) -> None:
+        """In place on the packed records (sums.py:309-316): the records are
+        transposed to device planes, conjugated, and written back."""
+        soa = self.to_soa()
+        soa.apply_clifford(gate, qubits)
+        if len(self):
+            x, z, f, _ = soa.columns()
+            self._data["x"], self._data["z"], self._data["flags"] = x, z, f
+
+    def apply_rotation(self, rot, *, eps: float = 0.0, combine: bool = True):
+        """sums.py:318-325."""
+        return self.to_soa().apply_rotation(rot, eps=eps, combine=combine).to_aos()
 
     def truncate(self, eps: float):
         if eps < 0:
