@@ -138,9 +138,62 @@ def c3(dev, flush):
                             "ms_per_step": t, "groups": int(ng.item()), "pair_checks": checks}}
 
 
+def f12(dev, flush):
+    """§8(f) rows: Clifford gates (f2) and the rotation split + merge (f1) on
+    C5-style sums (n=500, W=8), 2^24 terms for the gates (HBM roofline), 2^21
+    for the rotation."""
+    out = {}
+    M = 1 << 24
+    x, z, f, c = rng.random_columns(500, 1 << 16, 41)
+    S = pl.PauliSumSoA.from_columns(500, x, z, f, c, device=dev)
+    # tile the 2^16 drawn terms to 2^24 on the device (content is irrelevant to timing)
+    S.x = S.x.repeat(1, M >> 16).contiguous()
+    S.z = S.z.repeat(1, M >> 16).contiguous()
+    S.flags = S.flags.repeat(M >> 16).contiguous()
+    S.coeffs = S.coeffs.repeat(M >> 16).contiguous()
+    # algorithmic bytes per term: H reads x, z, phase of one word (17 B) and
+    # writes x, z (16 B) + the phase of Y terms (1/4); CNOT across two words
+    # reads 4 words + phase (33 B), writes x_t, z_c (16 B) + flipped phases (1/8)
+    for gate, q, bpt in (("H", 77, 33.25), ("CNOT", (3, 300), 49.125)):
+        ms = _timed(lambda: S.apply_clifford(gate, q), dev, flush, 10)
+        t = statistics.mean(ms)
+        byts = M * bpt
+        out[f"f2_clifford_{gate}"] = {
+            "workload": f"f2 apply_clifford {gate} on 2^24 terms, n=500",
+            "value": M / (t / 1e3), "unit": "terms/s", "ms_per_step": t,
+            "roofline": {"bound": "hbm", "achieved": byts / (t / 1e3) / 1e9, "peak": _hbm(),
+                         "unit": "GB/s", "frac": byts / (t / 1e3) / 1e9 / _hbm(),
+                         "bytes_per_unit": f"{bpt} B (touched words + phase, read + written)"}}
+    del S
+    torch.cuda.empty_cache()
+    m = 1 << 21
+    x, z, f, c = rng.random_columns(500, m, 42)
+    S = pl.PauliSumSoA.from_columns(500, x, z, f, c, device=dev)
+    gx, gz, _, _ = rng.random_columns(500, 1, 43)
+    rot = pl.RotationSpec(pl.PauliString(500, gx[0], gz[0], 0), 0.37)
+    raw = S.apply_rotation(rot, combine=False)
+    mo = len(raw)
+    del raw
+    ms = _timed(lambda: S.apply_rotation(rot, combine=False), dev, flush, 10)
+    t = statistics.mean(ms)
+    byts = m * (145 + 8) + mo * 145  # read terms + anti/scan words, write split terms
+    out["f1_rotation_split"] = {
+        "workload": "f1 rotation split (un-combined), 2^21 terms n=500, random generator",
+        "value": m / (t / 1e3), "unit": "input terms/s", "ms_per_step": t, "output_terms": mo,
+        "roofline": {"bound": "hbm", "achieved": byts / (t / 1e3) / 1e9, "peak": _hbm(),
+                     "unit": "GB/s", "frac": byts / (t / 1e3) / 1e9 / _hbm(),
+                     "bytes_per_unit": "145 B term read + 8 B flags/scan + 145 B per output term"}}
+    ms = _timed(lambda: S.apply_rotation(rot), dev, flush, 5)
+    t = statistics.mean(ms)
+    out["f1_apply_rotation"] = {
+        "workload": "f1 apply_rotation (split + sort_and_combine), 2^21 terms n=500",
+        "value": m / (t / 1e3), "unit": "input terms/s", "ms_per_step": t}
+    return out
+
+
 def run_secondary(dev, flush) -> dict:
     out = {}
-    for fn in (c2, c1, c5, c3):
+    for fn in (c2, c1, c5, c3, f12):
         try:
             r = fn(dev, flush)
         except Exception as e:  # keep the headline line even if a side metric fails
