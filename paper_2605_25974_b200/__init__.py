@@ -18,6 +18,7 @@ from .grouping import (CommutationPartition, GroupingStats, ValidationReport, gr
                        group_greedy, validate_partition)
 from .bitmatrix import commutation_bitmatrix, unpack_bits
 from .rotations import RotationSpec, TRIG_SNAP, reorder_rotation, trig_values
+from .hamio import HamiltonianFormatError, read_hamiltonian, write_hamiltonian
 from .rng import SplitMix64, config_columns, random_columns, random_sum
 from ._native import NativeLibraryError
 
@@ -35,6 +36,7 @@ __all__ = [
     "group_greedy", "validate_partition",
     "commutation_bitmatrix", "unpack_bits",
     "RotationSpec", "TRIG_SNAP", "reorder_rotation", "trig_values",
+    "HamiltonianFormatError", "read_hamiltonian", "write_hamiltonian",
     "SplitMix64", "config_columns", "random_columns", "random_sum",
     "NativeLibraryError", "__version__",
 ]

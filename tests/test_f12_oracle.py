@@ -79,3 +79,46 @@ def test_gate_validation():
         gates.check_gate("H", (1, 2), 10)
     with pytest.raises(ValueError):
         gates.check_gate("T", (1,), 10)
+
+
+# ------------------------------------------------------------------ f4 hamio
+def test_hamio_write_matches_reference():
+    import io
+
+    import paper_2605_25974_b200 as pl
+
+    g = golden("hamio_n12")
+    s = pl.PauliSum.from_columns(12, g["x0"], g["z0"], g["f0"], g["c0"])
+    buf = io.StringIO()
+    pl.write_hamiltonian(buf, s)
+    assert buf.getvalue() == str(g["text"])
+
+
+def test_hamio_read_matches_reference():
+    import io
+
+    import paper_2605_25974_b200 as pl
+
+    g = golden("hamio_n12")
+    s = pl.read_hamiltonian(io.StringIO(str(g["src"])))
+    x, z, f, c = s.columns()
+    assert np.array_equal(x, g["px"]) and np.array_equal(z, g["pz"])
+    assert np.array_equal(f, g["pf"]) and np.array_equal(c, g["pc"])
+
+
+@pytest.mark.parametrize("text,exc", [
+    ("1.0 0.0\n", "HamiltonianFormatError"),
+    ("1.0 abc XY\n", "HamiltonianFormatError"),
+    ("1.0 0.0 XY\n2.0 0.0 XYZ\n", "DimensionError"),
+    ("1.0 0.0 XQ\n", "HamiltonianFormatError"),
+    ("# nothing\n\n", "HamiltonianFormatError"),
+])
+def test_hamio_errors(text, exc):
+    import io
+
+    import paper_2605_25974_b200 as pl
+
+    with pytest.raises(getattr(pl, exc)) as e:
+        pl.read_hamiltonian(io.StringIO(text))
+    if exc == "HamiltonianFormatError":
+        assert e.value.line in (0, 1, 2)
