@@ -138,6 +138,24 @@ def c3(dev, flush):
                             "ms_per_step": t, "groups": int(ng.item()), "pair_checks": checks}}
 
 
+def f3(dev, flush):
+    """§8(f) row f3: two-phase parallel grouping of config 3 (8 chunks); the
+    partition differs from the sequential greedy one by design, so the group
+    count divergence is reported (bench.py:255-262 of the reference)."""
+    x, z, f, c = rng.config_columns(3)
+    S = pl.PauliSumSoA.from_columns(100, x, z, f, c, device=dev)
+    st = pl.GroupingStats()
+    part = pl.group_greedy_parallel(S, 8, stats=st)
+    ms = _timed(lambda: pl.group_greedy_parallel(S, 8), dev, flush, 2, warm=1)
+    t = statistics.mean(ms)
+    _, ng, _ = pl.group_assignment(S)
+    return {"f3_grouping_parallel": {
+        "workload": "f3 group_greedy_parallel, C3 (JW n=100, 10^5 terms), 8 chunks",
+        "value": st.pair_checks / (t / 1e3), "unit": "reference pair_checks/s", "ms_per_step": t,
+        "groups": part.group_count(), "groups_sequential_greedy": int(ng.item()),
+        "pair_checks": st.pair_checks}}
+
+
 def f12(dev, flush):
     """§8(f) rows: Clifford gates (f2) and the rotation split + merge (f1) on
     C5-style sums (n=500, W=8), 2^24 terms for the gates (HBM roofline), 2^21
@@ -193,7 +211,7 @@ def f12(dev, flush):
 
 def run_secondary(dev, flush) -> dict:
     out = {}
-    for fn in (c2, c1, c5, c3, f12):
+    for fn in (c2, c1, c5, c3, f12, f3):
         try:
             r = fn(dev, flush)
         except Exception as e:  # keep the headline line even if a side metric fails

@@ -207,6 +207,24 @@ int pl_group_greedy(int W, int64_t M, const uint64_t* x, const uint64_t* z, int6
                     void* workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------
+ * §8(f) f3 — merge phase of the two-phase parallel grouping.  Replaces the
+ * sequential merge of group_greedy_parallel (grouping.py:120-145): the local
+ * groups of the chunk-wise greedy runs (K6 on each contiguous chunk), listed
+ * in processing order as device `members` (term ids) with HOST offsets
+ * `local_off` [n_local + 1] (local_off[n_local] == M), each join the first
+ * global group (creation order) whose members all commute with theirs, else
+ * open a new one.  global_of_local (device, n_local) receives each local
+ * group's global id, *n_global (device) the global group count, and
+ * *pair_checks (device) is INCREASED by the reference's merge contribution
+ * (|local| * |group| per group tried).  Exact: same partition as the reference.
+ */
+int64_t pl_group_merge_workspace_bytes(int64_t M, int32_t n_local);
+int pl_group_merge(int W, int64_t M, const uint64_t* x, const uint64_t* z, int64_t ld,
+                   const int32_t* members, const int64_t* local_off, int32_t n_local,
+                   int32_t* global_of_local, int32_t* n_global, int64_t* pair_checks,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
  * §8(f) f2 — Clifford conjugation in place.  Replaces gates.py:72-102
  * (apply_clifford_inplace, called by _SumBase.apply_clifford, sums.py:309-316):
  * every term P becomes U P U^dagger for gate H (0), S (1), CNOT (2, q0 =

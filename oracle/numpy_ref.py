@@ -242,3 +242,33 @@ def rotation_split(x, z, flags, coeffs, gx, gz, cos_t: float, sin_t: float):
     oc[first] = np.where(anti, coeffs * cos_t, coeffs)
     ox[second], oz[second], of[second], oc[second] = x[anti] ^ gx, z[anti] ^ gz, 0, prod
     return ox, oz, of, oc
+
+
+def greedy_parallel(x, z, chunks: int):
+    """Two-phase grouping (grouping.py:98-146): greedy per contiguous chunk
+    (np.array_split), then each local group joins the first global group all
+    of whose cross pairs commute, else opens one.  Returns (groups in member
+    order, pair_checks)."""
+    m = x.shape[0]
+    pieces = [p for p in np.array_split(np.arange(m), chunks) if p.size]
+    checks = 0
+    locals_ = []
+    for p in pieces:
+        groups_l, c = greedy(x[p], z[p])
+        checks += int(c)
+        locals_.extend([[int(p[0]) + t for t in g] for g in groups_l])
+    glob: list[list[int]] = []
+    for loc in locals_:
+        lx, lz = x[loc], z[loc]
+        placed = False
+        for g in glob:
+            checks += len(loc) * len(g)
+            gx, gz = x[g], z[g]
+            cross = _pc(lx[:, None, :] & gz[None, :, :]) + _pc(lz[:, None, :] & gx[None, :, :])
+            if not (cross & 1).any():
+                g.extend(loc)
+                placed = True
+                break
+        if not placed:
+            glob.append(list(loc))
+    return glob, checks

@@ -15,7 +15,7 @@ from .strings import (PauliString, batch_multiply, batch_pair_multiply, batch_si
 from .sums import (PauliSum, PauliSumSoA, PauliTerm, outer_multiply, sort_and_combine,
                    sort_combine, sum_from_terms, sum_multiply, to_aos, to_soa, truncate)
 from .grouping import (CommutationPartition, GroupingStats, ValidationReport, group_assignment,
-                       group_greedy, validate_partition)
+                       group_greedy, group_greedy_parallel, validate_partition)
 from .bitmatrix import commutation_bitmatrix, unpack_bits
 from .rotations import RotationSpec, TRIG_SNAP, reorder_rotation, trig_values
 from .hamio import HamiltonianFormatError, read_hamiltonian, write_hamiltonian
@@ -33,7 +33,7 @@ __all__ = [
     "PauliSum", "PauliSumSoA", "PauliTerm", "outer_multiply", "sort_and_combine", "sort_combine",
     "sum_from_terms", "sum_multiply", "to_aos", "to_soa", "truncate",
     "CommutationPartition", "GroupingStats", "ValidationReport", "group_assignment",
-    "group_greedy", "validate_partition",
+    "group_greedy", "group_greedy_parallel", "validate_partition",
     "commutation_bitmatrix", "unpack_bits",
     "RotationSpec", "TRIG_SNAP", "reorder_rotation", "trig_values",
     "HamiltonianFormatError", "read_hamiltonian", "write_hamiltonian",

@@ -77,6 +77,8 @@ SIGNATURES = {
     "pl_merge_received": (_I, [C.POINTER(MergePlan), _P, _L, _P, _I, C.c_int32, C.c_int32,
                                _P, _P, _P, _P, _L, _P, _P, _P, _P, _L, _D, _P, _S,
                                _P, _P, _P, _P, _L, _P, _P]),
+    "pl_group_merge_workspace_bytes": (_L, [_L, C.c_int32]),
+    "pl_group_merge": (_I, [_I, _L, _P, _P, _L, _P, _P, C.c_int32, _P, _P, _P, _P, _S, _P]),
     "pl_apply_clifford": (_I, [_I, _L, _P, _P, _P, _L, _I, _I, _I, _P]),
     "pl_rotation_workspace_bytes": (_L, [_L]),
     "pl_rotation_split": (_I, [_I, _L, _P, _P, _P, _P, _L, _P, _P, _D, _D, _D, _P, _S, _P, _P, _P,

@@ -5,8 +5,10 @@ Mirrors ``paulialg/grouping.py``: :class:`GroupingStats` (:22-26),
 :func:`group_greedy` (:91-95), :func:`validate_partition` (:149-181).  The
 assignment is computed on the GPU by ``pl_group_greedy`` and is identical to
 the reference's sequential first-fit scan (:67-83), including the
-``pair_checks`` counter (:75-76).  ``group_greedy_parallel`` (the two-phase
-chunked variant, :98-146) is outside this build's hot-path scope.
+``pair_checks`` counter (:75-76).  :func:`group_greedy_parallel` (the two-phase
+chunked variant, :98-146, §8(f) row f3) runs K6 per contiguous chunk and the
+sequential merge on the GPU (``pl_group_merge``), reproducing the reference's
+partition (member order included) and its ``pair_checks``.
 """
 
 from __future__ import annotations
@@ -106,6 +108,78 @@ def group_greedy(s, *, stats: GroupingStats | None = None) -> CommutationPartiti
     if stats is not None:
         stats.pair_checks += int(pc.item())
     return part
+
+
+def _greedy_chunk(S, r0: int, r1: int, dev):
+    """K6 on terms [r0, r1) of the device planes S: (group_of, n_groups, pair_checks)."""
+    m = r1 - r0
+    gof = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+    ng = torch.zeros(1, dtype=torch.int32, device=dev)
+    pc = torch.zeros(1, dtype=torch.int64, device=dev)
+    lib = _native.load()
+    ws_bytes = int(lib.pl_group_workspace_bytes(S.W, m))
+    xv, zv = S.x[:, r0:r1], S.z[:, r0:r1]
+    for _ in range(6):
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+        with torch.cuda.device(dev):
+            rc = lib.pl_group_greedy(S.W, m, ptr(xv), ptr(zv), S.ld, ptr(gof), ptr(ng), ptr(pc),
+                                     ptr(ws), ws.numel(), stream_ptr(dev))
+        if rc != _PL_ERR_WORKSPACE:
+            _native.check(rc, "pl_group_greedy")
+            break
+        del ws
+        ws_bytes *= 4
+    else:
+        _native.check(rc, "pl_group_greedy")
+    return gof[:m], pc
+
+
+def group_greedy_parallel(s, chunks: int, *, stats: GroupingStats | None = None
+                          ) -> CommutationPartition:
+    """Two-phase grouping (grouping.py:98-146): greedy per contiguous chunk,
+    then a sequential merge of the local groups into global groups.  With
+    chunks=1 the partition equals group_greedy's."""
+    if chunks < 1:
+        raise ValueError("chunk count must be >= 1")
+    if not isinstance(s, PauliSumSoA):
+        s = s.to_soa()
+    dev, _ = _compute_device(s)
+    S = s.to(dev).planes()
+    m = S.M
+    pieces = [p for p in np.array_split(np.arange(m), chunks) if p.size]
+    locals_: list[list[int]] = []
+    checks = 0
+    for p in pieces:
+        r0, r1 = int(p[0]), int(p[-1]) + 1
+        gof, pc = _greedy_chunk(S, r0, r1, dev)
+        part = CommutationPartition.from_assignment(gof.cpu().numpy())
+        locals_.extend([[r0 + t for t in g] for g in part.groups])
+        checks += int(pc.item())
+    n_local = len(locals_)
+    if n_local == 0:
+        if stats is not None:
+            stats.pair_checks += checks
+        return CommutationPartition([], m)
+    members = torch.as_tensor(np.fromiter((t for g in locals_ for t in g), np.int32, m),
+                              device=dev)
+    off = np.zeros(n_local + 1, dtype=np.int64)
+    off[1:] = np.cumsum([len(g) for g in locals_])
+    gol = torch.empty(n_local, dtype=torch.int32, device=dev)
+    ng = torch.zeros(1, dtype=torch.int32, device=dev)
+    pc = torch.zeros(1, dtype=torch.int64, device=dev)
+    ws = torch.empty(int(_native.load().pl_group_merge_workspace_bytes(m, n_local)),
+                     dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        _native.call("pl_group_merge", S.W, m, ptr(S.x), ptr(S.z), S.ld, ptr(members),
+                     off.ctypes.data, n_local, ptr(gol), ptr(ng), ptr(pc), ptr(ws), ws.numel(),
+                     stream_ptr(dev))
+    gol_h = gol.cpu().numpy()
+    groups: list[list[int]] = [[] for _ in range(int(ng.item()))]
+    for g, local in zip(gol_h, locals_):
+        groups[int(g)].extend(local)
+    if stats is not None:
+        stats.pair_checks += checks + int(pc.item())
+    return CommutationPartition(groups, m)
 
 
 def validate_partition(s, p: CommutationPartition) -> ValidationReport:

@@ -122,3 +122,16 @@ def test_hamio_errors(text, exc):
         pl.read_hamiltonian(io.StringIO(text))
     if exc == "HamiltonianFormatError":
         assert e.value.line in (0, 1, 2)
+
+
+# ------------------------------------------------------------ f3 parallel grouping
+@pytest.mark.parametrize("name", ["group_par_rand", "group_par_dense", "group_par_jw"])
+@pytest.mark.parametrize("chunks", [1, 2, 5, 16])
+def test_oracle_greedy_parallel_golden(name, chunks):
+    g = golden(name)
+    groups, checks = R.greedy_parallel(g["x"], g["z"], chunks)
+    flat = [t for grp in groups for t in grp]
+    offs = np.cumsum([0] + [len(grp) for grp in groups])
+    assert np.array_equal(flat, g[f"members{chunks}"])
+    assert np.array_equal(offs, g[f"offsets{chunks}"])
+    assert checks == int(g[f"checks{chunks}"])

@@ -88,3 +88,42 @@ def test_all_commuting_one_group(cuda):
 def test_config3_full(cuda):
     x, z, _, _ = rng.config_columns(3)
     check_vs_oracle(100, x, z, cuda)
+
+
+# ------------------------------------------------------------ f3 parallel grouping
+@pytest.mark.parametrize("name", ["group_par_rand", "group_par_dense", "group_par_jw"])
+@pytest.mark.parametrize("chunks", [1, 2, 5, 16])
+def test_group_greedy_parallel_golden(cuda, name, chunks):
+    g = golden(name)
+    n = int(g["n"])
+    m = g["x"].shape[0]
+    s = pl.PauliSumSoA.from_columns(n, g["x"], g["z"], np.zeros(m, np.uint8),
+                                    np.ones(m, np.complex128), device=cuda)
+    st = pl.GroupingStats()
+    part = pl.group_greedy_parallel(s, chunks, stats=st)
+    flat = [t for grp in part.groups for t in grp]
+    assert np.array_equal(flat, g[f"members{chunks}"])
+    assert np.array_equal(np.cumsum([0] + [len(x) for x in part.groups]), g[f"offsets{chunks}"])
+    assert st.pair_checks == int(g[f"checks{chunks}"])
+    assert pl.validate_partition(s, part).ok
+
+
+def test_group_greedy_parallel_one_chunk_equals_greedy(cuda):
+    x, z, f, c = rng.config_columns(3, scale=0.05)
+    s = pl.PauliSumSoA.from_columns(100, x, z, f, c, device=cuda)
+    assert pl.group_greedy_parallel(s, 1).groups == pl.group_greedy(s).groups
+
+
+def test_group_greedy_parallel_matches_oracle_c3_prefix(cuda):
+    x, z, f, c = rng.config_columns(3, scale=0.1)
+    s = pl.PauliSumSoA.from_columns(100, x, z, f, c, device=cuda)
+    st = pl.GroupingStats()
+    part = pl.group_greedy_parallel(s, 8, stats=st)
+    groups, checks = R.greedy_parallel(x, z, 8)
+    assert part.groups == groups and st.pair_checks == checks
+
+
+def test_group_greedy_parallel_errors(cuda):
+    s = pl.PauliSumSoA.from_columns(10, *rng.random_columns(10, 4, 1), device=cuda)
+    with pytest.raises(ValueError):
+        pl.group_greedy_parallel(s, 0)
