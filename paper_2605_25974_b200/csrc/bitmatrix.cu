@@ -57,7 +57,7 @@ static int launch_bitmatrix(int64_t M, const u64* x, const u64* z, int64_t ld, i
     uint32_t* list = (uint32_t*)p;
     const int64_t cap = ((int64_t)ws_bytes - (p - (uint8_t*)ws)) / 4;
     const unsigned nb = (unsigned)ceil_div(rows, 256);
-    k_row_weight<W, 1><<<nb, 256, 0, st>>>(x, z, ld, row0, rows, off);
+    k_row_weight<W, 2><<<nb, 256, 0, st>>>(x, z, ld, row0, rows, off);
     PLB_CHECK_LAUNCH("k_row_weight");
     int rc = exclusive_scan_u32(off, off, rows, scratch, off + rows, st);
     if (rc) return rc;
@@ -75,25 +75,25 @@ static int launch_bitmatrix(int64_t M, const u64* x, const u64* z, int64_t ld, i
       }
       method = 2;
     } else {
-      k_row_fill<W, 1><<<nb, 256, 0, st>>>(x, z, ld, row0, rows, off, list);
+      k_row_fill<W, 2><<<nb, 256, 0, st>>>(x, z, ld, row0, rows, off, list);
       PLB_CHECK_LAUNCH("k_row_fill");
-      const int64_t colblocks = ceil_div(cols, kColsPerCta);
+      const int64_t colblocks = ceil_div(cols, kColsY);
       int64_t splits = ceil_div(2 * num_sms(), colblocks);
       const int64_t max_splits = ceil_div(rows, 256);
       if (splits > max_splits) splits = max_splits;
       if (splits < 1) splits = 1;
       if (splits > 65535) splits = 65535;
       const int64_t rps = ceil_div(rows, splits);
-      const size_t smem = lists64_smem_bytes<W>();
-      auto kern = k_bitmatrix_lists64<W>;
+      const size_t smem = letters_smem_bytes<W>();
+      auto kern = k_bitmatrix_letters<W>;
       PLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       for (int64_t cbase = 0; cbase < colblocks; cbase += 65535) {
         const int64_t nblk = colblocks - cbase < 65535 ? colblocks - cbase : 65535;
         dim3 grid((unsigned)nblk, (unsigned)splits);
-        StageTimer t_(st, "k_bitmatrix_lists64");
-        kern<<<grid, 1024, smem, st>>>(x, z, ld, M, row0, rows, col0 + cbase * kColsPerCta,
-                                       cols - cbase * kColsPerCta, off, list,
-                                       bits + cbase * (kColsPerCta / 32), ld_bits, rps);
+        StageTimer t_(st, "k_bitmatrix_letters");
+        kern<<<grid, 1024, smem, st>>>(x, z, ld, M, row0, rows, col0 + cbase * kColsY,
+                                       cols - cbase * kColsY, off, list,
+                                       bits + cbase * (kColsY / 32), ld_bits, rps);
         PLB_CHECK_LAUNCH("k_bitmatrix_lists");
       }
       return PL_OK;

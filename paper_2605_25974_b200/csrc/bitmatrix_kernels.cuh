@@ -24,8 +24,11 @@ __global__ void k_row_weight(const u64* __restrict__ x, const u64* __restrict__ 
   const int64_t r = row0 + i;
   int c = 0;
 #pragma unroll
-  for (int w = 0; w < W; ++w) c += popc64(__ldg(x + w * ld + r)) + popc64(__ldg(z + w * ld + r));
-  cnt[i] = FMT == 1 ? (uint32_t)((c + 3) & ~3) : (uint32_t)c;
+  for (int w = 0; w < W; ++w) {
+    const u64 xv = __ldg(x + w * ld + r), zv = __ldg(z + w * ld + r);
+    c += FMT == 2 ? popc64(xv | zv) : popc64(xv) + popc64(zv);  // FMT 2: one entry per letter
+  }
+  cnt[i] = FMT >= 1 ? (uint32_t)((c + 3) & ~3) : (uint32_t)c;
 }
 
 template <int W, int FMT = 0>
@@ -38,6 +41,27 @@ __global__ void k_row_fill(const u64* __restrict__ x, const u64* __restrict__ z,
   uint32_t o = off[i];
   uint16_t* l16 = reinterpret_cast<uint16_t*>(list_);
   uint32_t* l32 = reinterpret_cast<uint32_t*>(list_);
+  if (FMT == 2) {
+    // one entry per letter, byte offsets of 128-byte slice rows: X at q -> z
+    // slice q, Z -> x slice 64W + q, Y -> (z ^ x) slice 128W + q
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const u64 xv = __ldg(x + w * ld + r), zv = __ldg(z + w * ld + r);
+      const u64 cls[3] = {xv & ~zv, zv & ~xv, xv & zv};
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        u64 v = cls[k];
+        while (v) {
+          const int b = __ffsll((long long)v) - 1;
+          v &= v - 1;
+          l32[o++] = 128u * (uint32_t)(k * 64 * W + w * 64 + b);
+        }
+      }
+    }
+    const uint32_t end = off[i + 1];
+    while (o < end) l32[o++] = 128u * (uint32_t)(192 * W);
+    return;
+  }
 #pragma unroll
   for (int u = 0; u < 2 * W; ++u) {
     u64 v = u < W ? __ldg(x + u * ld + r) : __ldg(z + (u - W) * ld + r);
@@ -240,6 +264,131 @@ k_bitmatrix_lists64(const u64* __restrict__ x, const u64* __restrict__ z, int64_
     }
     __syncwarp();
   }
+}
+
+// ------------------- method 1, letter slices (fast path)
+// Per CTA 1024 columns; slices are stored entry-major as TY[e][h] (uint64, h =
+// 16 groups of 64 columns) for three entry kinds per qubit q: the z slice (a
+// row letter X at q), the x slice (Z) and their XOR (Y), so a row costs one
+// 64-bit shared load per letter instead of one per set bit.  Each warp stages
+// the entries of blocks of 16 rows and processes two rows per pass (half-warp
+// per row, each lane producing 64 column bits).
+constexpr int kColsY = 1024;
+constexpr int kRowsY = 16;     // rows staged per warp block
+constexpr int kEBufY = 240;    // staged entries per warp (<= 15 letters per row on average)
+
+template <int W>
+__global__ void __launch_bounds__(1024, 1)
+k_bitmatrix_letters(const u64* __restrict__ x, const u64* __restrict__ z, int64_t ld, int64_t M,
+                    int64_t row0, int64_t rows, int64_t col0, int64_t cols,
+                    const uint32_t* __restrict__ off, const uint32_t* __restrict__ list,
+                    uint32_t* __restrict__ bits, int64_t ld_bits, int64_t rows_per_split) {
+  constexpr int E = 192 * W;  // slices: z (64W) | x (64W) | z^x (64W), + sentinel
+  extern __shared__ __align__(16) uint32_t TY32[];  // [E+1][16] u64 | ebuf [32][kEBufY] u32
+  u64* TY = reinterpret_cast<u64*>(TY32);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c0 = col0 + (int64_t)blockIdx.x * kColsY;
+  {  // transpose: warp g ballots columns c0+32g.. -> h = g/2, 32-bit half g&1
+    const int64_t c = c0 + 32 * warp + lane;
+    const bool valid = c < col0 + cols && c < M;
+    const int h = warp >> 1, part = warp & 1;
+#pragma unroll 1
+    for (int u = 0; u < 2 * W; ++u) {
+      const u64 v = valid ? (u < W ? __ldg(z + u * ld + c) : __ldg(x + (u - W) * ld + c)) : 0ull;
+      uint32_t mlo = 0, mhi = 0;
+#pragma unroll
+      for (int b = 0; b < 32; ++b) {
+        const uint32_t m = __ballot_sync(0xffffffffu, (uint32_t)(v >> b) & 1u);
+        if (lane == b) mlo = m;
+      }
+#pragma unroll
+      for (int b = 0; b < 32; ++b) {
+        const uint32_t m = __ballot_sync(0xffffffffu, (uint32_t)(v >> (32 + b)) & 1u);
+        if (lane == b) mhi = m;
+      }
+      TY32[((u * 64 + lane) * 16 + h) * 2 + part] = mlo;
+      TY32[((u * 64 + 32 + lane) * 16 + h) * 2 + part] = mhi;
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 64 * W * 16; t += blockDim.x) {  // Y slices
+    const int q = t >> 4, h = t & 15;
+    TY[(128 * W + q) * 16 + h] = TY[q * 16 + h] ^ TY[(64 * W + q) * 16 + h];
+  }
+  if (threadIdx.x < 16) TY[E * 16 + threadIdx.x] = 0ull;  // sentinel slice
+  __syncthreads();
+  const int words_here = (int)ceil_div(cols - (c0 - col0) < kColsY ? cols - (c0 - col0) : kColsY,
+                                       32);
+  const int64_t wcol = (c0 - col0) / 32;
+  const int half = lane >> 4, hl = lane & 15;
+  const uint32_t tb = (uint32_t)__cvta_generic_to_shared(TY) + (uint32_t)(hl * 8);
+  const int64_t r_begin = (int64_t)blockIdx.y * rows_per_split;
+  int64_t r_end = r_begin + rows_per_split;
+  if (r_end > rows) r_end = rows;
+  constexpr int kTBytes = (((E + 1) * 16 * 8 + 15) / 16) * 16;
+  uint32_t* ebuf = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(TY32) + kTBytes) +
+                   warp * kEBufY;
+  const uint32_t ebuf_s = (uint32_t)__cvta_generic_to_shared(ebuf);
+  const bool w0 = 2 * hl < words_here, w1 = 2 * hl + 1 < words_here;
+  const int64_t nblk = ceil_div(r_end - r_begin, kRowsY);
+  for (int64_t blk = warp; blk < nblk; blk += 32) {
+    const int64_t rb = r_begin + blk * kRowsY;
+    const int nr = (int)(r_end - rb < kRowsY ? r_end - rb : kRowsY);
+    const uint32_t my_off = lane <= nr ? off[rb + lane] : 0u;  // lane nr holds the block end
+    const uint32_t o_first = __shfl_sync(0xffffffffu, my_off, 0);
+    const uint32_t o_end = __shfl_sync(0xffffffffu, my_off, nr);
+    const uint32_t total = o_end - o_first;  // multiple of 4
+    const bool staged = total <= (uint32_t)kEBufY;
+    if (staged) {
+      const uint4* srcl = reinterpret_cast<const uint4*>(list + o_first);
+      uint4* dst = reinterpret_cast<uint4*>(ebuf);
+      for (uint32_t k = lane; k < total / 4; k += 32) dst[k] = srcl[k];
+      __syncwarp();
+    }
+    for (int j = 0; j < nr; j += 2) {
+      const int jr = j + half;  // this half-warp's row
+      const uint32_t a = __shfl_sync(0xffffffffu, my_off, jr & 31);
+      const uint32_t bnx = __shfl_sync(0xffffffffu, my_off, (jr + 1) & 31);
+      const bool live = jr < nr;
+      const uint32_t beg = live ? a - o_first : 0u;
+      const uint32_t end = live ? bnx - o_first : 0u;
+      unsigned long long acc = 0;
+      if (staged) {
+        uint4 e = make_uint4(0, 0, 0, 0);
+        if (beg < end)
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w)
+                       : "r"(ebuf_s + 4 * beg));
+        unsigned long long acc1 = 0;
+        for (uint32_t k = beg; k < end; k += 4) {
+          uint4 en = e;
+          if (k + 4 < end)
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(en.x), "=r"(en.y), "=r"(en.z), "=r"(en.w)
+                         : "r"(ebuf_s + 4 * (k + 4)));
+          const unsigned long long t0 = lds64(tb + e.x), t1 = lds64(tb + e.y);
+          const unsigned long long t2 = lds64(tb + e.z), t3 = lds64(tb + e.w);
+          acc ^= t0 ^ t1;
+          acc1 ^= t2 ^ t3;
+          e = en;
+        }
+        acc ^= acc1;
+      } else {
+        for (uint32_t k = beg; k < end; ++k) acc ^= lds64(tb + list[o_first + k]);
+      }
+      if (live) {
+        uint32_t* out = bits + (rb + jr) * ld_bits + wcol + 2 * hl;
+        if (w0) out[0] = (uint32_t)acc;
+        if (w1) out[1] = (uint32_t)(acc >> 32);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int W>
+constexpr size_t letters_smem_bytes() {
+  return (size_t)((((192 * W + 1) * 16 * 8) + 15) / 16) * 16 + (size_t)32 * kEBufY * 4;
 }
 
 // dynamic shared memory of the list kernels
