@@ -331,20 +331,57 @@ k_bitmatrix_letters(const u64* __restrict__ x, const u64* __restrict__ z, int64_
   const uint32_t ebuf_s = (uint32_t)__cvta_generic_to_shared(ebuf);
   const bool w0 = 2 * hl < words_here, w1 = 2 * hl + 1 < words_here;
   const int64_t nblk = ceil_div(r_end - r_begin, kRowsY);
-  for (int64_t blk = warp; blk < nblk; blk += 32) {
+  // Software pipeline over this warp's row blocks (blk, blk+32, ...): the
+  // offsets of block i+2 and the entries of block i+1 are loaded into
+  // registers while block i is computed from the staged entries.
+  constexpr int kEVec = kEBufY / 4 / 32 + 1;  // uint4 entry vectors per lane (>= kEBufY/4/32)
+  auto load_off = [&](int64_t blk) -> uint32_t {
+    if (blk >= nblk) return 0u;
     const int64_t rb = r_begin + blk * kRowsY;
     const int nr = (int)(r_end - rb < kRowsY ? r_end - rb : kRowsY);
-    const uint32_t my_off = lane <= nr ? off[rb + lane] : 0u;  // lane nr holds the block end
+    return lane <= nr ? __ldg(off + rb + lane) : 0u;  // lane nr holds the block end
+  };
+  auto block_nr = [&](int64_t blk) -> int {
+    const int64_t rb = r_begin + blk * kRowsY;
+    return (int)(r_end - rb < kRowsY ? r_end - rb : kRowsY);
+  };
+  auto load_entries = [&](int64_t blk, uint32_t offv, uint4 (&ev)[kEVec]) {
+    if (blk >= nblk) return;
+    const int nr = block_nr(blk);
+    const uint32_t o_first = __shfl_sync(0xffffffffu, offv, 0);
+    const uint32_t total = __shfl_sync(0xffffffffu, offv, nr) - o_first;
+    if (total > (uint32_t)kEBufY) return;
+    const uint4* srcl = reinterpret_cast<const uint4*>(list + o_first);
+#pragma unroll
+    for (int v = 0; v < kEVec; ++v) {
+      const uint32_t k = lane + 32 * v;
+      if (k < total / 4) ev[v] = __ldg(srcl + k);
+    }
+  };
+  uint32_t off_cur = load_off(warp);
+  uint32_t off_nxt = load_off(warp + 32);
+  uint4 ev[kEVec];
+  load_entries(warp, off_cur, ev);
+  for (int64_t blk = warp; blk < nblk; blk += 32) {
+    const int64_t rb = r_begin + blk * kRowsY;
+    const int nr = block_nr(blk);
+    const uint32_t my_off = off_cur;
     const uint32_t o_first = __shfl_sync(0xffffffffu, my_off, 0);
     const uint32_t o_end = __shfl_sync(0xffffffffu, my_off, nr);
     const uint32_t total = o_end - o_first;  // multiple of 4
     const bool staged = total <= (uint32_t)kEBufY;
     if (staged) {
-      const uint4* srcl = reinterpret_cast<const uint4*>(list + o_first);
       uint4* dst = reinterpret_cast<uint4*>(ebuf);
-      for (uint32_t k = lane; k < total / 4; k += 32) dst[k] = srcl[k];
+#pragma unroll
+      for (int v = 0; v < kEVec; ++v) {
+        const uint32_t k = lane + 32 * v;
+        if (k < total / 4) dst[k] = ev[v];
+      }
       __syncwarp();
     }
+    // prefetch: offsets two blocks ahead, entries of the next block
+    const uint32_t off_nn = load_off(blk + 64);
+    load_entries(blk + 32, off_nxt, ev);
     for (int j = 0; j < nr; j += 2) {
       const int jr = j + half;  // this half-warp's row
       const uint32_t a = __shfl_sync(0xffffffffu, my_off, jr & 31);
@@ -383,6 +420,8 @@ k_bitmatrix_letters(const u64* __restrict__ x, const u64* __restrict__ z, int64_
       }
     }
     __syncwarp();
+    off_cur = off_nxt;
+    off_nxt = off_nn;
   }
 }
 
