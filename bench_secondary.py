@@ -184,10 +184,12 @@ def f12(dev, flush):
                          "bytes_per_unit": f"{bpt} B (touched words + phase, read + written)"}}
     del S
     torch.cuda.empty_cache()
+    # Pauli-propagation-like inputs: config-5 style terms (weight 2-12 over
+    # 500 qubits) and a sparse generator
     m = 1 << 21
-    x, z, f, c = rng.random_columns(500, m, 42)
+    x, z, f, c = rng.c5_columns(m, seed=42)
     S = pl.PauliSumSoA.from_columns(500, x, z, f, c, device=dev)
-    gx, gz, _, _ = rng.random_columns(500, 1, 43)
+    gx, gz, _, _ = rng.c5_columns(1, seed=43)
     rot = pl.RotationSpec(pl.PauliString(500, gx[0], gz[0], 0), 0.37)
     raw = S.apply_rotation(rot, combine=False)
     mo = len(raw)
@@ -196,7 +198,7 @@ def f12(dev, flush):
     t = statistics.mean(ms)
     byts = m * (145 + 8) + mo * 145  # read terms + anti/scan words, write split terms
     out["f1_rotation_split"] = {
-        "workload": "f1 rotation split (un-combined), 2^21 terms n=500, random generator",
+        "workload": "f1 rotation split (un-combined), 2^21 C5-style terms n=500, sparse generator",
         "value": m / (t / 1e3), "unit": "input terms/s", "ms_per_step": t, "output_terms": mo,
         "roofline": {"bound": "hbm", "achieved": byts / (t / 1e3) / 1e9, "peak": _hbm(),
                      "unit": "GB/s", "frac": byts / (t / 1e3) / 1e9 / _hbm(),
@@ -204,7 +206,7 @@ def f12(dev, flush):
     ms = _timed(lambda: S.apply_rotation(rot), dev, flush, 5)
     t = statistics.mean(ms)
     out["f1_apply_rotation"] = {
-        "workload": "f1 apply_rotation (split + sort_and_combine), 2^21 terms n=500",
+        "workload": "f1 apply_rotation (split + sort_and_combine), 2^21 C5-style terms n=500",
         "value": m / (t / 1e3), "unit": "input terms/s", "ms_per_step": t}
     return out
 

@@ -30,7 +30,7 @@ extern "C" int pl_outer_plan(int W, int64_t Ma, int64_t Mb, const uint64_t* ax,
   plan->ma = Ma;
   plan->mb = Mb;
   plan->n_items = Ma * Mb;
-  u64 masks[32] = {0};
+  u64 masks[2 * PL_PLAN_MAX_SEG + 1] = {0};
   int rc = compute_masks(W, (const u64*)ax, (const u64*)az, lda, Ma, (const u64*)bx,
                          (const u64*)bz, ldb, Mb, masks, (cudaStream_t)stream);
   if (rc) return rc;
@@ -54,7 +54,7 @@ extern "C" int pl_sort_plan(int W, int64_t M, const uint64_t* x, const uint64_t*
   plan->ma = M;
   plan->mb = 1;
   plan->n_items = M;
-  u64 masks[32] = {0};
+  u64 masks[2 * PL_PLAN_MAX_SEG + 1] = {0};
   int rc = compute_masks(W, (const u64*)x, (const u64*)z, ld, M, nullptr, nullptr, 0, 0, masks,
                          (cudaStream_t)stream);
   if (rc) return rc;

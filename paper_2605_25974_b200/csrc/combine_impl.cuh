@@ -60,6 +60,11 @@ constexpr int kSplitTileThreads = 256;
 struct Layout {
   int W, KW, active;  // active: bit w set if z-word w or x-word w is used
   int lo[PL_PLAN_MAX_SEG], len[PL_PLAN_MAX_SEG], pos[PL_PLAN_MAX_SEG];
+  // sparse keys (wide, sparse sort keys): the key is the list of the packed
+  // key's set-bit positions p, most significant first, each stored as the
+  // sbits-wide value key_bits - p, terminated by 0; lexicographic order on
+  // these slot sequences equals the packed keys' order
+  int sparse, sbits, nslots, key_bits;
 };
 
 struct Ctl {  // control arrays inside the workspace
@@ -157,6 +162,23 @@ __device__ __forceinline__ void pack_key(const Layout& L, const u64 (&zc)[W], co
                                          u64 (&key)[KW]) {
 #pragma unroll
   for (int d = 0; d < KW; ++d) key[d] = 0;
+  if (L.sparse) {
+    int k = 0;
+#pragma unroll
+    for (int s = 0; s < 2 * W; ++s) {
+      const int len = L.len[s];
+      if (!len) continue;
+      u64 w = ((s < W ? zc[s] : xc[s - W]) >> L.lo[s]) & low_mask(len);
+      while (w) {  // segment bits, most significant first
+        const int hb = 63 - __clzll((long long)w);
+        w ^= 1ull << hb;
+        const int p = L.pos[s] + (len - 1 - hb);
+        put_seg<KW>(key, (u64)(L.key_bits - p), k * L.sbits, L.sbits);
+        ++k;
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int s = 0; s < 2 * W; ++s) {
     const int len = L.len[s];
@@ -165,6 +187,31 @@ __device__ __forceinline__ void pack_key(const Layout& L, const u64 (&zc)[W], co
       put_seg<KW>(key, (w >> L.lo[s]) & low_mask(len), L.pos[s], len);
     }
   }
+}
+
+// Plane word q of a sparse key staged at KS[d * T + e], consuming the slots
+// from cursor k on (planes are visited in order, so every slot whose position
+// precedes plane q's range was consumed by an earlier plane).
+__device__ __forceinline__ u64 sparse_plane_next(const Layout& L, const u64* KS, int T, int e,
+                                                 int q, int& k) {
+  const int len = L.len[q];
+  const int lo = L.pos[q], hi = L.pos[q] + len;
+  u64 w = 0;
+  for (; k < L.nslots; ++k) {
+    const int bit = k * L.sbits, wi = bit >> 6, off = bit & 63;
+    const u64 a = KS[wi * T + e];
+    const u64 b = off + L.sbits > 64 ? KS[(wi + 1) * T + e] : 0ull;
+    const u64 hiw = off ? ((a << off) | (b >> (64 - off))) : a;
+    const u64 v = hiw >> (64 - L.sbits);
+    if (v == 0) {
+      k = L.nslots;
+      break;
+    }
+    const int p = L.key_bits - (int)v;
+    if (p >= hi) break;
+    w |= 1ull << (L.lo[q] + len - 1 - (p - lo));
+  }
+  return w;
 }
 
 template <int KW>
@@ -1044,6 +1091,23 @@ static void finish_plan(pl_merge_plan* P, const u64* masks /* z[W] then x[W] */)
   P->key_bits = pos;
   P->key_words = key_words_for_bits(pos > 0 ? pos : 1);
   P->reserved[0] = active;
+  // sort_and_combine of wide, sparse keys: the set-bit position list is
+  // shorter than the packed bit string (config 5: 1000-bit keys with <= 24
+  // set bits -> 250 bits, KW 16 -> 4)
+  P->reserved[4] = P->reserved[5] = P->reserved[6] = 0;
+  if (P->mode == 1 && pos > 0) {
+    const int maxbits = (int)masks[2 * W];
+    int sb = 1;
+    while ((1 << sb) <= pos) ++sb;  // values key_bits - p in [1, key_bits]
+    const int nslots = maxbits + 1;  // + the 0 terminator
+    const int kw_sparse = key_words_for_bits(nslots * sb);
+    if (kw_sparse < P->key_words) {
+      P->key_words = kw_sparse;
+      P->reserved[4] = 1;
+      P->reserved[5] = sb;
+      P->reserved[6] = nslots;
+    }
+  }
   const int KW = P->key_words;
   const int cap = leaf_cap_for(KW);
   P->leaf_cap = cap;
@@ -1074,16 +1138,27 @@ template <int W>
 __global__ void k_or_masks(const u64* __restrict__ x, const u64* __restrict__ z, int64_t ld,
                            int64_t m, u64* out) {
   u64 mz[W], mx[W];
+  unsigned long long maxbits = 0;  // most set bits (x and z) of any term
 #pragma unroll
   for (int w = 0; w < W; ++w) mz[w] = mx[w] = 0;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m;
        t += (int64_t)gridDim.x * blockDim.x) {
+    int bitsum = 0;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      mz[w] |= z[w * ld + t];
-      mx[w] |= x[w * ld + t];
+      const u64 zv = z[w * ld + t], xv = x[w * ld + t];
+      mz[w] |= zv;
+      mx[w] |= xv;
+      bitsum += popc64(zv) + popc64(xv);
     }
+    maxbits = maxbits > (unsigned long long)bitsum ? maxbits : (unsigned long long)bitsum;
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, maxbits, o);
+    maxbits = v > maxbits ? v : maxbits;
+  }
+  if ((threadIdx.x & 31) == 0 && maxbits) atomicMax(&out[2 * W], maxbits);
 #pragma unroll
   for (int w = 0; w < W; ++w) {
 #pragma unroll
@@ -1127,18 +1202,19 @@ static int compute_masks(int W, const u64* x1, const u64* z1, int64_t ld1, int64
   }
   std::lock_guard<std::mutex> lock(mtx);
   if (!dbuf[dev]) {
-    PLB_CUDA(cudaMalloc((void**)&dbuf[dev], 2 * PL_PLAN_MAX_SEG * sizeof(u64)));
-    PLB_CUDA(cudaMallocHost((void**)&hbuf[dev], 2 * PL_PLAN_MAX_SEG * sizeof(u64)));
+    PLB_CUDA(cudaMalloc((void**)&dbuf[dev], (2 * PL_PLAN_MAX_SEG + 1) * sizeof(u64)));
+    PLB_CUDA(cudaMallocHost((void**)&hbuf[dev], (2 * PL_PLAN_MAX_SEG + 1) * sizeof(u64)));
   }
   u64* dmask = dbuf[dev];
-  PLB_CUDA(cudaMemsetAsync(dmask, 0, 2 * W * sizeof(u64), st));
+  PLB_CUDA(cudaMemsetAsync(dmask, 0, (2 * W + 1) * sizeof(u64), st));
   int rc = PLB_DISPATCH_W(W, launch_masks, x1, z1, ld1, m1, dmask, st);
   if (rc == PL_OK && x2) rc = PLB_DISPATCH_W(W, launch_masks, x2, z2, ld2, m2, dmask, st);
   if (rc == PL_OK) {
-    PLB_CUDA(cudaMemcpyAsync(hbuf[dev], dmask, 2 * W * sizeof(u64), cudaMemcpyDeviceToHost, st));
+    PLB_CUDA(cudaMemcpyAsync(hbuf[dev], dmask, (2 * W + 1) * sizeof(u64), cudaMemcpyDeviceToHost,
+                             st));
   }
   PLB_CUDA(cudaStreamSynchronize(st));
-  if (rc == PL_OK) memcpy(host_masks, hbuf[dev], 2 * W * sizeof(u64));
+  if (rc == PL_OK) memcpy(host_masks, hbuf[dev], (2 * W + 1) * sizeof(u64));
   return rc;
 }
 
@@ -1147,6 +1223,10 @@ static Layout to_layout(const pl_merge_plan& P) {
   L.W = P.W;
   L.KW = P.key_words;
   L.active = (int)P.reserved[0];
+  L.sparse = (int)P.reserved[4];
+  L.sbits = (int)P.reserved[5];
+  L.nslots = (int)P.reserved[6];
+  L.key_bits = P.key_bits;
   for (int s = 0; s < PL_PLAN_MAX_SEG; ++s) {
     L.lo[s] = P.seg_lo[s];
     L.len[s] = P.seg_len[s];

@@ -591,7 +591,7 @@ __host__ __device__ constexpr size_t leaf_sort_smem_bytes(int KW) {
 // DRAM sector is written whole exactly once.
 constexpr int kEmitThreads = 256;
 __host__ __device__ constexpr int emit_tile(int KW) {
-  return KW <= 2 ? 2048 : KW <= 4 ? 1024 : KW <= 8 ? 512 : KW <= 16 ? 256 : 128;
+  return KW <= 2 ? 2048 : KW <= 4 ? 1024 : KW <= 8 ? 512 : 256;  // >= kEmitThreads
 }
 __host__ __device__ constexpr size_t emit_smem_bytes(int KW) {
   return (size_t)emit_tile(KW) * (8 * KW + 16) + (size_t)kEmitThreads * 12 + 64;
@@ -669,6 +669,11 @@ k_emit(Layout L, Dims D, Ctl C, OutP O) {
       __syncthreads();
     }
     // plane-major stores: each plane gets T*8 contiguous bytes from this CTA
+    // (sparse keys: the slots are sorted by packed position and the planes
+    // cover ascending position ranges, so one cursor per term walks them once)
+    int cur[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) cur[u] = 0;
     for (int q = 0; q < 2 * W; ++q) {
       const int len = L.len[q];
       u64* dst = (q < W ? O.oz + (int64_t)q * O.ldo : O.ox + (int64_t)(q - W) * O.ldo) + o0;
@@ -679,7 +684,9 @@ k_emit(Layout L, Dims D, Ctl C, OutP O) {
         const int e = u * kEmitThreads + tid;
         if ((uint32_t)o0 + e >= o1) break;
         u64 w = 0;
-        if (len) {
+        if (L.sparse) {
+          if (len) w = sparse_plane_next(L, KS, T, e, q, cur[u]);
+        } else if (len) {
           const u64 a = KS[wi * T + e];
           const u64 b = (off && wi + 1 < KW) ? KS[(wi + 1) * T + e] : 0ull;
           const u64 hi = off ? ((a << off) | (b >> (64 - off))) : a;

@@ -241,3 +241,47 @@ def test_buckets_balanced(cuda):
     cnt = counts.cpu().numpy()
     assert cnt.sum() == A.M * B.M
     assert cnt.max() < 4 * cnt.mean(), (cnt.max(), cnt.mean())
+
+
+def test_sparse_keys_plan_and_parity(cuda):
+    """Wide sparse keys (config 5 style) take the set-bit-list key encoding
+    (KW 16 -> 4) and still merge exactly; negated duplicates cancel."""
+    x, z, f, c = rng.c5_columns(50_000, seed=9)
+    x = np.concatenate([x, x[:5000]])
+    z = np.concatenate([z, z[:5000]])
+    f = np.concatenate([f, f[:5000]])
+    c = np.concatenate([c, -c[:5000]])  # exact cancellations
+    out = pl.sort_and_combine(soa(500, (x, z, f, c), cuda))
+    assert pl.sums.LAST_PLAN["key_words"] < 16
+    check_combined(out, R.combine(x, z, f, c))
+
+
+@pytest.mark.parametrize("n", [200, 1000])
+def test_sparse_keys_other_tiers(cuda, n):
+    r = np.random.default_rng(n)
+    W = pl.words_for(n)
+    m = 20_000
+    x = np.zeros((m, W), np.uint64)
+    z = np.zeros((m, W), np.uint64)
+    for t in range(m):  # weight-3 strings, many repeats
+        for q in r.choice(n, 3, replace=False) if t % 3 else [1, 2, 3]:
+            ltr = r.integers(1, 4)
+            if ltr & 1:
+                x[t, q // 64] |= np.uint64(1) << np.uint64(q % 64)
+            if ltr & 2:
+                z[t, q // 64] |= np.uint64(1) << np.uint64(q % 64)
+    f = r.integers(0, 4, m).astype(np.uint8)
+    c = (r.normal(size=m) + 1j * r.normal(size=m)).astype(np.complex128)
+    out = pl.sort_and_combine(soa(n, (x, z, f, c), cuda))
+    check_combined(out, R.combine(x, z, f, c))
+
+
+def test_dense_keys_w16_sort(cuda):
+    """n = 1000 uniform random strings: ~1500 set bits per key, dense KW=32 path."""
+    x, z, f, c = rng.random_columns(1000, 3000, 5)
+    x = np.concatenate([x, x[:100]])
+    z = np.concatenate([z, z[:100]])
+    f = np.concatenate([f, f[:100]])
+    c = np.concatenate([c, c[:100]])
+    out = pl.sort_and_combine(soa(1000, (x, z, f, c), cuda))
+    check_combined(out, R.combine(x, z, f, c))
