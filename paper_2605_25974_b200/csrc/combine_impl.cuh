@@ -52,6 +52,7 @@ constexpr int kSortSmemBytes = 200 * 1024;
 constexpr int kSampleOversample = 16;  // level-2 samples per sub-bucket
 constexpr int kSample1Oversample = 16;  // level-1 samples per bucket
 constexpr int kLeavesPerBucket = 32;
+constexpr int kTabBits = 13;  // level-1 prefix table: splitters per top-13-bit key prefix
 constexpr int kMaxBuckets = 2048;
 constexpr int kSplitTile = 4096;     // items per level-2 classification tile
 constexpr int kSplitTileThreads = 256;
@@ -88,6 +89,7 @@ struct Ctl {  // control arrays inside the workspace
   uint32_t* rmap;         // emit range -> first leaf
   u64* opk;               // [KW][ma (+ mb)] packed operand keys
   uint8_t* opb;           // [ma (+ mb)] operand base phases
+  uint16_t* l1tab;        // 2^kTabBits + 1: first splitter per top-bit prefix
   u64* k1;               // [KW][n] item keys, buffer 1
   uint32_t* i1;          // [n]
   u64* k2;               // buffer 2
@@ -474,6 +476,24 @@ k_sample(Layout L, Dims D, SrcA S, Ctl C) {
   }
 }
 
+// level-1 prefix table: tab[h] = number of splitters whose top kTabBits bits
+// are < h (h = 0 .. 2^kTabBits); a key with prefix h lies after splitter
+// tab[h]-1 and before splitter tab[h+1], so only [tab[h], tab[h+1]) is searched
+template <int KW>
+__global__ void k_l1_table(Dims D, Ctl C) {
+  const int nsp = D.nb1 - 1;
+  for (int h = blockIdx.x * blockDim.x + threadIdx.x; h <= (1 << kTabBits);
+       h += gridDim.x * blockDim.x) {
+    int lo = 0, hi = nsp;  // first splitter with prefix >= h
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((int64_t)(C.split[mid] >> (64 - kTabBits)) < (int64_t)h) lo = mid + 1;
+      else hi = mid;
+    }
+    C.l1tab[h] = (uint16_t)lo;
+  }
+}
+
 // ---------------------------------------------------- 2./4. count, scatter
 // Packing is a fixed bit permutation, so it commutes with XOR: the key of the
 // product a_i*b_j is pack(a_i) ^ pack(b_j).  k_pack_ops packs every operand
@@ -517,6 +537,7 @@ struct GenSmem {
   u64* tkey;       // outer: [KW][kGenTB] packed b-term keys
   uint32_t* tpb;   // outer: [kGenTB] b-term base phases
   uint32_t* slot;  // per item: bucket << 16 | rank  (scatter only)
+  uint16_t* tab;   // level-1 prefix table (2^kTabBits + 1)
 };
 
 template <int W>
@@ -529,16 +550,19 @@ __device__ __forceinline__ GenSmem gen_smem(u64* sm, int nb1, int KW) {
   g.tkey = g.tile + 2 * W * kGenTB;
   g.tpb = reinterpret_cast<uint32_t*>(g.tkey + KW * kGenTB);
   g.slot = g.tpb + kGenTB;
+  g.tab = reinterpret_cast<uint16_t*>(g.slot + kGenTB * kGenThreads);
   return g;
 }
 
 __host__ __device__ constexpr size_t gen_smem_bytes(int W, int KW, int nb1) {
   return (size_t)8 * KW * nb1 + 8 * (size_t)nb1 + (size_t)16 * W * kGenTB +
-         (size_t)8 * KW * kGenTB + 4 * (size_t)kGenTB + (size_t)4 * kGenTB * kGenThreads + 64;
+         (size_t)8 * KW * kGenTB + 4 * (size_t)kGenTB + (size_t)4 * kGenTB * kGenThreads +
+         2 * (size_t)((1 << kTabBits) + 1) + 64;
 }
 
 template <int KW>
 __device__ __forceinline__ void gen_prologue(const GenSmem& g, const Ctl& C, int nb1) {
+  for (int h = threadIdx.x; h <= (1 << kTabBits); h += blockDim.x) g.tab[h] = C.l1tab[h];
   for (int b = threadIdx.x; b < nb1; b += blockDim.x) {
     g.hist[b] = 0;
     if (b < nb1 - 1) {
@@ -652,7 +676,6 @@ k_count(Layout L, Dims D, SrcA S, Ctl C) {
   Gen<W, KW, MODE> gen;
   gen.init(L, D, S, C, g);
   __syncthreads();
-  const int nsp = D.nb1 - 1, top = pow2_floor(nsp);
 #pragma unroll 1
   for (int j0 = 0; j0 < kGenTB; j0 += kGenIlp) {
     u64 key[kGenIlp][KW];
@@ -664,11 +687,25 @@ k_count(Layout L, Dims D, SrcA S, Ctl C) {
       ok[u] = gen.item(L, D, C, g, j0 + u, key[u], ik);
       pos[u] = 0;
     }
-    for (int step = top; step > 0; step >>= 1) {
+    // the prefix table narrows each search to the splitters sharing the
+    // key's top kTabBits bits (usually none or a few)
+    int hi[kGenIlp], step[kGenIlp];
+    int smax = 0;
+#pragma unroll
+    for (int u = 0; u < kGenIlp; ++u) {
+      const int h = (int)(key[u][0] >> (64 - kTabBits));
+      pos[u] = g.tab[h];
+      hi[u] = g.tab[h + 1];
+      step[u] = pow2_floor(hi[u] - pos[u]);
+      smax = step[u] > smax ? step[u] : smax;
+    }
+    for (int st = smax; st > 0; st >>= 1) {
 #pragma unroll
       for (int u = 0; u < kGenIlp; ++u) {
-        const int c = pos[u] + step;
-        if (c <= nsp && !key_lt<KW>(key[u], g.split, D.nb1, c - 1)) pos[u] = c;
+        if (step[u] >= st) {
+          const int c = pos[u] + st;
+          if (c <= hi[u] && !key_lt<KW>(key[u], g.split, D.nb1, c - 1)) pos[u] = c;
+        }
       }
     }
 #pragma unroll
@@ -681,7 +718,7 @@ k_count(Layout L, Dims D, SrcA S, Ctl C) {
 }
 
 template <int W, int KW, int MODE>
-__global__ void __launch_bounds__(kGenThreads)
+__global__ void __launch_bounds__(kGenThreads, 3)
 k_scatter(Layout L, Dims D, SrcA S, Ctl C) {
   extern __shared__ u64 sm[];
   const GenSmem g = gen_smem<W>(sm, D.nb1, KW);
@@ -689,7 +726,6 @@ k_scatter(Layout L, Dims D, SrcA S, Ctl C) {
   Gen<W, KW, MODE> gen;
   gen.init(L, D, S, C, g);
   __syncthreads();
-  const int nsp = D.nb1 - 1, top = pow2_floor(nsp);
 #pragma unroll 1
   for (int j0 = 0; j0 < kGenTB; j0 += kGenIlp) {
     u64 key[kGenIlp][KW];
@@ -701,11 +737,25 @@ k_scatter(Layout L, Dims D, SrcA S, Ctl C) {
       ok[u] = gen.item(L, D, C, g, j0 + u, key[u], ik);
       pos[u] = 0;
     }
-    for (int step = top; step > 0; step >>= 1) {
+    // the prefix table narrows each search to the splitters sharing the
+    // key's top kTabBits bits (usually none or a few)
+    int hi[kGenIlp], step[kGenIlp];
+    int smax = 0;
+#pragma unroll
+    for (int u = 0; u < kGenIlp; ++u) {
+      const int h = (int)(key[u][0] >> (64 - kTabBits));
+      pos[u] = g.tab[h];
+      hi[u] = g.tab[h + 1];
+      step[u] = pow2_floor(hi[u] - pos[u]);
+      smax = step[u] > smax ? step[u] : smax;
+    }
+    for (int st = smax; st > 0; st >>= 1) {
 #pragma unroll
       for (int u = 0; u < kGenIlp; ++u) {
-        const int c = pos[u] + step;
-        if (c <= nsp && !key_lt<KW>(key[u], g.split, D.nb1, c - 1)) pos[u] = c;
+        if (step[u] >= st) {
+          const int c = pos[u] + st;
+          if (c <= hi[u] && !key_lt<KW>(key[u], g.split, D.nb1, c - 1)) pos[u] = c;
+        }
       }
     }
 #pragma unroll
@@ -1023,7 +1073,7 @@ static inline int64_t align256(int64_t v) { return (v + 255) & ~(int64_t)255; }
 
 struct WsLayout {
   int64_t split, bcount, bbase, bcursor, leaf_off, n_leaves, leaf_ctr, tile_off, n_tiles,
-      sub_count, leaf_desc, split2, kept, kprefix, scan, k1, i1, k2, i2, sums, rmap, opk, opb, total;
+      sub_count, leaf_desc, split2, kept, kprefix, scan, k1, i1, k2, i2, sums, rmap, opk, opb, l1tab, total;
 };
 
 // Bound on the number of leaves: a bucket of s items gets at most
@@ -1064,6 +1114,7 @@ static WsLayout ws_layout(const pl_merge_plan& P) {
   w.rmap = o; o = align256(o + 4 * (n / 128 + 2));
   w.opk = o; o = align256(o + 8 * KW * (P.ma + P.mb));
   w.opb = o; o = align256(o + (P.ma + P.mb));
+  w.l1tab = o; o = align256(o + 2 * ((1 << kTabBits) + 1));
   w.total = o;
   (void)ctl_end;
   return w;
@@ -1276,6 +1327,7 @@ static Ctl to_ctl(const pl_merge_plan& P, void* ws) {
   C.rmap = (uint32_t*)(b + w.rmap);
   C.opk = (u64*)(b + w.opk);
   C.opb = (uint8_t*)(b + w.opb);
+  C.l1tab = (uint16_t*)(b + w.l1tab);
   C.k1 = (u64*)(b + w.k1);
   C.i1 = (uint32_t*)(b + w.i1);
   C.k2 = (u64*)(b + w.k2);
@@ -1308,6 +1360,8 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const O
     k_sample<W, KW, MODE><<<1, kLeafThreads, sm1, st>>>(L, D, S, C);
     PLB_CHECK_LAUNCH("k_sample");
   }
+  k_l1_table<KW><<<((1 << kTabBits) + 256) / 256, 256, 0, st>>>(D, C);
+  PLB_CHECK_LAUNCH("k_l1_table");
   const size_t gsm = gen_smem_bytes(W, KW, D.nb1);
   dim3 ggrid;
   if (MODE == 0) ggrid = dim3((unsigned)ceil_div(D.ma, kGenThreads), (unsigned)ceil_div(D.mb, kGenTB));
@@ -1439,6 +1493,8 @@ static int run_partition(const pl_merge_plan& P, const SrcA& S, int64_t j0, int6
       k_sample<W, KW, 0><<<1, kLeafThreads, sm1, st>>>(L, D, S, C);
       PLB_CHECK_LAUNCH("k_sample");
     }
+    k_l1_table<KW><<<((1 << kTabBits) + 256) / 256, 256, 0, st>>>(D, C);
+    PLB_CHECK_LAUNCH("k_l1_table");
     const size_t gsm = gen_smem_bytes(W, KW, D.nb1);
     const dim3 ggrid((unsigned)ceil_div(D.ma, kGenThreads), (unsigned)ceil_div(D.mb, kGenTB));
     if (D.nb1 > 1) {
