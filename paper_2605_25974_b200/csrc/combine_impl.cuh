@@ -47,7 +47,7 @@ namespace plb {
 constexpr int kGenThreads = 256;
 constexpr int kGenTB = 16;        // b-terms per tile (outer) / terms per thread (sort)
 constexpr int kLeafThreads = 512;
-constexpr int kSplitThreads = 512;
+constexpr int kSplitThreads = 1024;
 constexpr int kSortSmemBytes = 200 * 1024;
 constexpr int kSampleOversample = 16;  // level-2 samples per sub-bucket
 constexpr int kSample1Oversample = 16;  // level-1 samples per bucket
