@@ -1,18 +1,19 @@
 // K5 — all-pairs commutation bitmatrix (restates grouping.py:136-140, the
 // parity popc(x_r & z_c) + popc(z_r & x_c) of strings.py:47-51).
 //
-// Method 1 (row-list XOR over transposed column slices).  A CTA owns a block
-// of 1024 columns and transposes it in shared memory into bit slices
-//   T[g][e]  (g = 32-column group, e = key bit),  bit t of T[g][e] = bit e of
-//   column c0 + 32g + t,  where e = 64u + b addresses z-word u (u < W) or
-//   x-word u - W (u >= W) of the column.
-// A row r anti-commutes with column c iff the XOR over the row's set bits of
-// the swapped partner slice is 1:   sip(r, c) = XOR_{b in x_r} z_c[b] ^
-// XOR_{b in z_r} x_c[b].  Each warp takes one row (its set-bit list is warp
-// uniform, so there is no divergence) and every lane produces 32 column bits
-// with one LDS + one XOR per set bit: cost per 1024 checks is proportional to
-// the row weight, which makes sparse Hamiltonians (config 5, weight 2-12)
-// bound by the 1-bit-per-check output stream instead of the INT pipe.
+// Method 1 (row-list XOR over transposed letter slices, the default for
+// sparse rows).  A CTA owns a block of 1024 columns and transposes it in
+// shared memory into three bit slices per qubit q: the columns' z bits at q,
+// their x bits at q, and the XOR of both.  A row letter X at q pairs with the
+// z slice, Z with the x slice and Y with the z^x slice, so
+//   sip(r, c) = XOR over the letters of r of the matching slice bit of c,
+// one 64-bit shared load + XOR per letter per 64 columns (a half-warp per
+// row, 16 lanes x 64 columns).  The rows' letter lists (CSR, built once per
+// call) are staged per warp 16 rows at a time and prefetched one block
+// ahead.  Cost per 1024 checks is proportional to the row weight (config 5:
+// weight 2-12), far below the 4W LOP3 + POPC per check of method 2; the
+// tensor-core formulation (int8 expansions, K = 128W) would cost 2048 ops per
+// check and is not used.
 //
 // Method 2 (direct).  One thread per row, the row's 2W words in registers,
 // columns broadcast from shared memory: 4W LOP3 + POPC per check.  Used for

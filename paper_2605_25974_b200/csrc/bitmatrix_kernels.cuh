@@ -11,11 +11,11 @@ constexpr int kTPad = 1;           // row pad of T (conflict-free lane reads)
 constexpr int kEBuf = 1024;        // per-warp staged entries of 32 rows (uint16)
 
 // ---------------------------------------------------------------- CSR lists
-// Entry e = 64u + b for set bit b of canonical word u (u < W: x word u,
-// u >= W: z word u - W).  FMT 0: uint16 entries e.  FMT 1 (bitmatrix fast
-// path): uint32 entries 128e (byte offset of slice row e of the 64-column
-// layout), every row padded to a multiple of 4 entries with the all-zero
-// sentinel slice E = 128W.
+// FMT 0 (grouping): uint16 entry e = 64u + b for set bit b of canonical word
+// u (u < W: x word u, u >= W: z word u - W).  FMT 2 (bitmatrix letter
+// kernel): one uint32 entry per letter, the byte offset of its slice row (z,
+// x or z^x slice of the qubit), every row padded to a multiple of 4 entries
+// with the all-zero sentinel slice 192W.
 template <int W, int FMT = 0>
 __global__ void k_row_weight(const u64* __restrict__ x, const u64* __restrict__ z, int64_t ld,
                              int64_t row0, int64_t rows, uint32_t* __restrict__ cnt) {
@@ -28,7 +28,7 @@ __global__ void k_row_weight(const u64* __restrict__ x, const u64* __restrict__ 
     const u64 xv = __ldg(x + w * ld + r), zv = __ldg(z + w * ld + r);
     c += FMT == 2 ? popc64(xv | zv) : popc64(xv) + popc64(zv);  // FMT 2: one entry per letter
   }
-  cnt[i] = FMT >= 1 ? (uint32_t)((c + 3) & ~3) : (uint32_t)c;
+  cnt[i] = FMT == 2 ? (uint32_t)((c + 3) & ~3) : (uint32_t)c;
 }
 
 template <int W, int FMT = 0>
@@ -68,13 +68,8 @@ __global__ void k_row_fill(const u64* __restrict__ x, const u64* __restrict__ z,
     while (v) {
       const int b = __ffsll((long long)v) - 1;
       v &= v - 1;
-      if (FMT == 1) l32[o++] = 128u * (uint32_t)(u * 64 + b);
-      else l16[o++] = (uint16_t)(u * 64 + b);
+      l16[o++] = (uint16_t)(u * 64 + b);
     }
-  }
-  if (FMT == 1) {
-    const uint32_t end = off[i + 1];
-    while (o < end) l32[o++] = 128u * (uint32_t)(128 * W);
   }
 }
 
@@ -149,120 +144,6 @@ k_bitmatrix_lists(const u64* __restrict__ x, const u64* __restrict__ z, int64_t 
       for (uint32_t k = 0; k < n; ++k) acc ^= Tl[__shfl_sync(0xffffffffu, e_l, k)];
     }
     if (lane < words_here) bits[i * ld_bits + wcol + lane] = acc;
-  }
-}
-
-// ---------------------------------- method 1, 64-column slices (fast path)
-// Slices are stored entry-major as T64[e][h] (uint64, h = 16 half-lanes):
-// bit t of T64[e][h] = key bit e of column c0 + 64h + t.  Each warp takes
-// blocks of 32 consecutive rows (offsets and FMT-1 entries staged into a
-// per-warp buffer with coalesced copies) and processes two rows per pass:
-// half-warp 0 row 2j, half-warp 1 row 2j+1, every lane producing 64 column
-// bits per entry with one 64-bit shared load at (slice base + entry).
-constexpr int kEBuf4 = 512;  // uint32 staged entries per warp
-
-template <int W>
-__global__ void __launch_bounds__(1024, 1)
-k_bitmatrix_lists64(const u64* __restrict__ x, const u64* __restrict__ z, int64_t ld, int64_t M,
-                    int64_t row0, int64_t rows, int64_t col0, int64_t cols,
-                    const uint32_t* __restrict__ off, const uint32_t* __restrict__ list,
-                    uint32_t* __restrict__ bits, int64_t ld_bits, int64_t rows_per_split) {
-  constexpr int E = 128 * W;
-  extern __shared__ __align__(16) uint32_t T32[];  // [E+1][16] u64 | ebuf [32][kEBuf4] u32
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t c0 = col0 + (int64_t)blockIdx.x * kColsPerCta;
-  {  // transpose: warp g ballots columns c0+32g.. -> half h = g/2, 32-bit half g&1
-    const int64_t c = c0 + 32 * warp + lane;
-    const bool valid = c < col0 + cols && c < M;
-    const int h = warp >> 1, part = warp & 1;
-#pragma unroll 1
-    for (int u = 0; u < 2 * W; ++u) {
-      const u64 v = valid ? (u < W ? __ldg(z + u * ld + c) : __ldg(x + (u - W) * ld + c)) : 0ull;
-      uint32_t mlo = 0, mhi = 0;
-#pragma unroll
-      for (int b = 0; b < 32; ++b) {
-        const uint32_t m = __ballot_sync(0xffffffffu, (uint32_t)(v >> b) & 1u);
-        if (lane == b) mlo = m;
-      }
-#pragma unroll
-      for (int b = 0; b < 32; ++b) {
-        const uint32_t m = __ballot_sync(0xffffffffu, (uint32_t)(v >> (32 + b)) & 1u);
-        if (lane == b) mhi = m;
-      }
-      T32[((u * 64 + lane) * 16 + h) * 2 + part] = mlo;
-      T32[((u * 64 + 32 + lane) * 16 + h) * 2 + part] = mhi;
-    }
-    if (lane == 0) T32[(E * 16 + h) * 2 + part] = 0;  // sentinel slice
-  }
-  __syncthreads();
-  const int words_here = (int)ceil_div(cols - (c0 - col0) < kColsPerCta ? cols - (c0 - col0)
-                                                                        : kColsPerCta, 32);
-  const int64_t wcol = (c0 - col0) / 32;
-  const int half = lane >> 4, hl = lane & 15;
-  const uint32_t tb = (uint32_t)__cvta_generic_to_shared(T32) + (uint32_t)(hl * 8);
-  const int64_t r_begin = (int64_t)blockIdx.y * rows_per_split;
-  int64_t r_end = r_begin + rows_per_split;
-  if (r_end > rows) r_end = rows;
-  constexpr int kTBytes = (((E + 1) * 16 * 8 + 15) / 16) * 16;
-  uint32_t* ebuf = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(T32) + kTBytes) +
-                   warp * kEBuf4;
-  const uint32_t ebuf_s = (uint32_t)__cvta_generic_to_shared(ebuf);
-  const bool w0 = 2 * hl < words_here, w1 = 2 * hl + 1 < words_here;
-  const int64_t nblk = ceil_div(r_end - r_begin, 32);
-  for (int64_t blk = warp; blk < nblk; blk += 32) {
-    const int64_t rb = r_begin + blk * 32;
-    const int nr = (int)(r_end - rb < 32 ? r_end - rb : 32);
-    const uint32_t my_off = lane < nr ? off[rb + lane] : 0u;
-    const uint32_t o_end = off[rb + nr];
-    const uint32_t o_first = __shfl_sync(0xffffffffu, my_off, 0);
-    const uint32_t total = o_end - o_first;  // multiple of 4
-    const bool staged = total <= (uint32_t)kEBuf4;
-    if (staged) {
-      const uint4* src = reinterpret_cast<const uint4*>(list + o_first);
-      uint4* dst = reinterpret_cast<uint4*>(ebuf);
-      for (uint32_t k = lane; k < total / 4; k += 32) dst[k] = src[k];
-      __syncwarp();
-    }
-    for (int j = 0; j < nr; j += 2) {
-      const int jr = j + half;  // this half-warp's row
-      const uint32_t a = __shfl_sync(0xffffffffu, my_off, jr & 31);
-      const uint32_t bnx = __shfl_sync(0xffffffffu, my_off, (jr + 1) & 31);
-      const bool live = jr < nr;
-      const uint32_t beg = live ? a - o_first : 0u;
-      const uint32_t end = live ? (jr + 1 < nr ? bnx : o_end) - o_first : 0u;
-      unsigned long long acc = 0;
-      if (staged) {
-        // entries for the next step are loaded before the current slices are
-        // consumed, so the entry -> slice load chain overlaps across steps
-        uint4 e = make_uint4(0, 0, 0, 0);
-        if (beg < end)
-          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                       : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w)
-                       : "r"(ebuf_s + 4 * beg));
-        unsigned long long acc1 = 0;
-        for (uint32_t k = beg; k < end; k += 4) {
-          uint4 en = e;
-          if (k + 4 < end)
-            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(en.x), "=r"(en.y), "=r"(en.z), "=r"(en.w)
-                         : "r"(ebuf_s + 4 * (k + 4)));
-          const unsigned long long t0 = lds64(tb + e.x), t1 = lds64(tb + e.y);
-          const unsigned long long t2 = lds64(tb + e.z), t3 = lds64(tb + e.w);
-          acc ^= t0 ^ t1;
-          acc1 ^= t2 ^ t3;
-          e = en;
-        }
-        acc ^= acc1;
-      } else {
-        for (uint32_t k = beg; k < end; ++k) acc ^= lds64(tb + list[o_first + k]);
-      }
-      if (live) {
-        uint32_t* out = bits + (rb + jr) * ld_bits + wcol + 2 * hl;
-        if (w0) out[0] = (uint32_t)acc;
-        if (w1) out[1] = (uint32_t)(acc >> 32);
-      }
-    }
-    __syncwarp();
   }
 }
 
@@ -435,11 +316,6 @@ template <int W>
 constexpr size_t lists_smem_bytes() {
   return (size_t)32 * (128 * W + kTPad) * 4;
 }
-template <int W>
-constexpr size_t lists64_smem_bytes() {
-  return (size_t)((((128 * W + 1) * 16 * 8) + 15) / 16) * 16 + (size_t)32 * kEBuf4 * 4;
-}
-
 // --------------------------------------------------------- method 2 kernel
 constexpr int kDirectRows = 256;  // one row per thread
 template <int W> struct DirectCols { static constexpr int value = W >= 16 ? 128 : 256; };

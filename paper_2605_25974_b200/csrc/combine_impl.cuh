@@ -650,19 +650,6 @@ struct Gen {
   }
 };
 
-// number of splitters <= key, branch-free with a fixed step count (all lanes
-// take the same path); top = largest power of two <= nsp (0 if nsp == 0)
-template <int KW>
-__device__ __forceinline__ int bucket_fixed(const u64 (&key)[KW], const u64* s, int64_t stride,
-                                            int nsp, int top) {
-  int pos = 0;
-  for (int step = top; step > 0; step >>= 1) {
-    const int c = pos + step;
-    if (c <= nsp && !key_lt<KW>(key, s, stride, c - 1)) pos = c;
-  }
-  return pos;
-}
-
 __device__ __forceinline__ int pow2_floor(int v) { return v > 0 ? 1 << (31 - __clz(v)) : 0; }
 
 constexpr int kGenIlp = 4;  // independent items per thread in flight
@@ -1055,15 +1042,6 @@ static int launch_split(const pl_merge_plan& P, const Dims& D, const Ctl& C, cud
 __device__ __forceinline__ bool keep_sum(double2 s, double eps) {
   if (eps == 0.0) return s.x != 0.0 || s.y != 0.0;
   return hypot(s.x, s.y) > eps;
-}
-
-__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 #include "merge_leaves.cuh"

@@ -38,21 +38,6 @@ __host__ __device__ constexpr size_t radix_smem_bytes(int cap) {
 
 
 
-template <int KW>
-__device__ __forceinline__ void cmp_swap(u64* K, uint32_t* I, int64_t stride, int i, int p) {
-  if (item_lt<KW>(K, I, stride, p, i)) {
-#pragma unroll
-    for (int d = 0; d < KW; ++d) {
-      const u64 t = K[d * stride + i];
-      K[d * stride + i] = K[d * stride + p];
-      K[d * stride + p] = t;
-    }
-    const uint32_t t = I[i];
-    I[i] = I[p];
-    I[p] = t;
-  }
-}
-
 // Straight-line compare-exchange with a compile-time stride: both items are
 // loaded once, compared branch-free and written back only when out of order.
 template <int KW, int STRIDE>
@@ -395,20 +380,6 @@ __device__ __noinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint8_t
   }
   __syncthreads();
   return true;
-}
-
-template <int W, int KW>
-__device__ __forceinline__ void write_term(const Layout& L, const OutP& O, uint64_t pos,
-                                           const u64 (&key)[KW], double2 s) {
-#pragma unroll
-  for (int q = 0; q < 2 * W; ++q) {
-    const int len = L.len[q];
-    const u64 w = len ? (get_seg<KW>(key, L.pos[q], len) << L.lo[q]) : 0ull;
-    if (q < W) O.oz[q * O.ldo + pos] = w;
-    else O.ox[(q - W) * O.ldo + pos] = w;
-  }
-  O.ok[pos] = 0;
-  O.oc[pos] = s;
 }
 
 // ------------------------------------------------------------ leaf sort
