@@ -556,16 +556,44 @@ __host__ __device__ constexpr size_t leaf_sort_smem_bytes(int KW) {
 // ------------------------------------------------------------ emit
 // Streams the merged terms out in output order: a CTA owns the output range
 // [o0, o0 + T) (T = emit_tile(KW) terms), finds the leaves covering it
-// (binary search on the kept-count prefix), stages the range's (key, sum)
-// entries in shared memory, then writes the SoA output one plane at a time --
-// each plane store of the CTA is T*8 contiguous bytes, aligned, so every
-// DRAM sector is written whole exactly once.
+// (range map + binary search on the kept-count prefix), stages the range's
+// (key, sum) entries in shared memory, then builds the SoA output one plane
+// at a time in a double-buffered shared tile that a TMA bulk store
+// (cp.async.bulk) writes out: T*8 contiguous, 16-byte aligned bytes per plane
+// per CTA, so every DRAM sector is written whole exactly once and the SM does
+// not issue the global stores itself.  The coefficients go out of the staging
+// buffer the same way and the phase bytes from a zero tile.  Partial (last)
+// tiles and unaligned outputs use plain coalesced stores.
 constexpr int kEmitThreads = 256;
 __host__ __device__ constexpr int emit_tile(int KW) {
-  return KW <= 2 ? 2048 : KW <= 4 ? 1024 : KW <= 8 ? 512 : 256;  // >= kEmitThreads
+  return KW <= 4 ? 1024 : KW <= 8 ? 512 : 256;  // >= kEmitThreads
 }
+// staged (key, sum) | leaf metadata | two plane buffers + zero phase bytes
+// for the TMA bulk stores
 __host__ __device__ constexpr size_t emit_smem_bytes(int KW) {
-  return (size_t)emit_tile(KW) * (8 * KW + 16) + (size_t)kEmitThreads * 12 + 64;
+  return (size_t)emit_tile(KW) * (8 * KW + 16) + (size_t)kEmitThreads * 12 + 64 +
+         (size_t)emit_tile(KW) * (2 * 8 + 1) + 16;
+}
+
+// TMA (cp.async.bulk) store of `bytes` from shared to global memory, one
+// bulk group per call (issued by one thread)
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+               "cp.async.bulk.commit_group;" ::"l"(gdst),
+               "r"((uint32_t)__cvta_generic_to_shared(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_le1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // last leaf l in [lo, hi] with pre[l] <= v (pre non-decreasing, pre[lo] <= v)
@@ -603,12 +631,25 @@ k_emit(Layout L, Dims D, Ctl C, OutP O) {
   uint32_t* m_pre = reinterpret_cast<uint32_t*>(SS + T);     // leaf chunk metadata
   uint32_t* m_end = m_pre + kEmitThreads;
   uint32_t* m_src = m_end + kEmitThreads;                    // buffer << 31 | offset
+  u64* PB = reinterpret_cast<u64*>(
+      (reinterpret_cast<uintptr_t>(m_src + kEmitThreads) + 15) & ~(uintptr_t)15);  // [2][T]
+  uint8_t* ZB = reinterpret_cast<uint8_t*>(PB + 2 * T);      // [T] zero phase bytes
   const int tid = threadIdx.x;
   const uint32_t n_leaves = *C.n_leaves;
   const uint32_t total = *C.scan_total;
   if (blockIdx.x == 0 && tid == 0) *O.count = (int64_t)total;
+  for (int e = tid; e < T; e += kEmitThreads) ZB[e] = 0;
+  fence_async_smem();
+  // full tiles go out through TMA bulk stores when every destination is
+  // 16-byte aligned (planes: even leading dimension)
+  const bool bulk_ok = ((reinterpret_cast<uintptr_t>(O.oz) | reinterpret_cast<uintptr_t>(O.ox) |
+                         reinterpret_cast<uintptr_t>(O.oc) | reinterpret_cast<uintptr_t>(O.ok)) &
+                        15) == 0 && (O.ldo & 1) == 0;
   for (uint64_t o0 = (uint64_t)blockIdx.x * T; o0 < total; o0 += (uint64_t)gridDim.x * T) {
     const uint32_t o1 = (uint32_t)(o0 + T < total ? o0 + T : total);
+    const bool bulk = bulk_ok && o1 - (uint32_t)o0 == (uint32_t)T;
+    if (tid == 0) bulk_wait_read_all();  // previous tile's bulk stores done reading KS/SS/PB
+    __syncthreads();
     const uint32_t r = (uint32_t)(o0 / T);
     const uint32_t l0 = C.rmap[r];
     const uint32_t l1 = o1 < total ? C.rmap[r + 1] : n_leaves - 1;
@@ -650,6 +691,11 @@ k_emit(Layout L, Dims D, Ctl C, OutP O) {
       u64* dst = (q < W ? O.oz + (int64_t)q * O.ldo : O.ox + (int64_t)(q - W) * O.ldo) + o0;
       const int pos = L.pos[q], lo = L.lo[q];
       const int wi = pos >> 6, off = pos & 63;
+      u64* pb = PB + (q & 1) * T;
+      if (bulk && q >= 2) {  // plane buffer q&1 free once the store of plane q-2 has read it
+        if (tid == 0) bulk_wait_read_le1();
+        __syncthreads();
+      }
 #pragma unroll
       for (int u = 0; u < PER; ++u) {
         const int e = u * kEmitThreads + tid;
@@ -663,8 +709,23 @@ k_emit(Layout L, Dims D, Ctl C, OutP O) {
           const u64 hi = off ? ((a << off) | (b >> (64 - off))) : a;
           w = (hi >> (64 - len)) << lo;
         }
-        dst[e] = w;
+        if (bulk) pb[e] = w;
+        else dst[e] = w;
       }
+      if (bulk) {
+        fence_async_smem();
+        __syncthreads();
+        if (tid == 0) bulk_store(dst, pb, (uint32_t)T * 8);
+      }
+    }
+    if (bulk) {  // coefficients straight from the staging buffer, phases from zeros
+      fence_async_smem();
+      __syncthreads();
+      if (tid == 0) {
+        bulk_store(O.oc + o0, SS, (uint32_t)T * 16);
+        bulk_store(O.ok + o0, ZB, (uint32_t)T);
+      }
+      continue;
     }
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
@@ -682,6 +743,7 @@ k_emit(Layout L, Dims D, Ctl C, OutP O) {
     }
     __syncthreads();
   }
+  if (tid == 0) bulk_wait_all();
 }
 
 template <int W, int KW, int MODE>
@@ -708,7 +770,7 @@ static int launch_leaves(const Layout& L, const Dims& D, const SrcA& S, const Ct
   if (esm > 48 * 1024)
     PLB_CUDA(cudaFuncSetAttribute(ke, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm));
   StageTimer t_(st, "k_emit");
-  ke<<<(unsigned)(3 * num_sms()), kEmitThreads, esm, st>>>(L, D, C, O);
+  ke<<<(unsigned)(4 * num_sms()), kEmitThreads, esm, st>>>(L, D, C, O);
   PLB_CHECK_LAUNCH("k_emit");
   return PL_OK;
 }
