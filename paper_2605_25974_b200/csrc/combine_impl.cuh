@@ -54,7 +54,7 @@ constexpr int kSample1Oversample = 16;  // level-1 samples per bucket
 constexpr int kLeavesPerBucket = 32;
 constexpr int kTabBits = 13;  // level-1 prefix table: splitters per top-13-bit key prefix
 constexpr int kMaxBuckets = 2048;
-constexpr int kSplitTile = 4096;     // items per level-2 classification tile
+constexpr int kSplitTile = 1024;     // items per level-2 classification tile
 constexpr int kSplitTileThreads = 256;
 
 // ---------------------------------------------------------------- layout
