@@ -285,3 +285,29 @@ def test_dense_keys_w16_sort(cuda):
     c = np.concatenate([c, c[:100]])
     out = pl.sort_and_combine(soa(1000, (x, z, f, c), cuda))
     check_combined(out, R.combine(x, z, f, c))
+
+
+def test_leaf_window_ties_fall_back(cuda):
+    """Keys that agree on the 24-bit radix window below the leaf's highest
+    differing bit but differ further down: the tie segments exceed the
+    insertion-sort limit and the leaf takes the bitonic fallback."""
+    r = np.random.default_rng(11)
+    m = 600
+    x = np.zeros((m, 1), np.uint64)
+    z = np.zeros((m, 1), np.uint64)
+    z[0, 0] = np.uint64(1) << np.uint64(63)  # a different high key bit
+    z[1:, 0] = np.uint64(1)                  # shared z part
+    x[1:, 0] = r.integers(0, 1 << 20, m - 1).astype(np.uint64)  # low bits differ
+    f = r.integers(0, 4, m).astype(np.uint8)
+    c = (r.normal(size=m) + 1j * r.normal(size=m)).astype(np.complex128)
+    out = pl.sort_and_combine(soa(64, (x, z, f, c), cuda))
+    check_combined(out, R.combine(x, z, f, c))
+
+
+def test_eps_drop_large(cuda):
+    """eps drops on a 10^6-product outer product (strict > eps keeps)."""
+    a, b = rng.config_columns(2)
+    eps = 0.5
+    out = pl.sum_multiply(soa(500, a, cuda), soa(500, b, cuda), eps=eps)
+    exp = R.outer_combine(*a, *b, eps=eps)
+    check_combined(out, exp)
