@@ -1,4 +1,4 @@
-import sys, time, torch, collections
+import sys, time, torch
 sys.path.insert(0, '.')
 import paper_2605_25974_b200 as pl
 from paper_2605_25974_b200 import rng, _native
@@ -8,10 +8,11 @@ S = pl.PauliSumSoA.from_columns(100, x, z, f, c, device=dev)
 for it in range(3):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     _native.stage_timing(True)
-    g, ng, pc = pl.group_assignment(S)
+    st = pl.GroupingStats()
+    p = pl.group_greedy_parallel(S, 8, stats=st)
     torch.cuda.synchronize(); t1 = time.perf_counter()
     _native.stage_timing(False)
-    agg = collections.defaultdict(float); cnt = collections.Counter()
-    for n, m in _native.stage_times():
-        agg[n] += m; cnt[n] += 1
-    print(it, 'wall %.1f ms' % ((t1 - t0) * 1e3), int(ng.item()), {k: (round(v, 2), cnt[k]) for k, v in agg.items()}, flush=True)
+    ts = _native.stage_times()
+    agg = {}
+    for n, m in ts: agg[n] = agg.get(n, 0) + m
+    print(it, 'wall %.1f ms' % ((t1 - t0) * 1e3), p.group_count(), st.pair_checks, {k: round(v, 2) for k, v in agg.items()}, flush=True)
