@@ -1,5 +1,5 @@
 import sys, time, torch
-sys.path.insert(0, '.')
+sys.path.insert(0, str(__import__('pathlib').Path(__file__).resolve().parents[2]))
 import paper_2605_25974_b200 as pl
 from paper_2605_25974_b200 import rng, _native
 dev = torch.device('cuda', 0)

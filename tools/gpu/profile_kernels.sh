@@ -1,4 +1,4 @@
-# usage: bash scratch/run_prof.sh <kernel-regex> <name> [count]
+# usage: bash tools/gpu/profile_kernels.sh <kernel-regex> <name> [count]
 RE="$1"; NAME="$2"; CNT="${3:-1}"
 CMD="python tools/gpu/probe_step.py"
 $CMD > gpurun_out/${NAME}_plain.log 2>&1 || { echo "plain run failed"; exit 1; }
