@@ -311,3 +311,29 @@ def test_eps_drop_large(cuda):
     out = pl.sum_multiply(soa(500, a, cuda), soa(500, b, cuda), eps=eps)
     exp = R.outer_combine(*a, *b, eps=eps)
     check_combined(out, exp)
+
+
+def test_sparse_keys_oversized_run(cuda):
+    """One sparse key repeated 3000 times (longer than a leaf) among config-5
+    terms: the in-place global-memory leaf path with set-bit-list keys."""
+    x, z, f, c = rng.c5_columns(20_000, seed=21)
+    rep = 3000
+    x = np.concatenate([x, np.repeat(x[7:8], rep, axis=0)])
+    z = np.concatenate([z, np.repeat(z[7:8], rep, axis=0)])
+    f = np.concatenate([f, np.full(rep, 1, np.uint8)])
+    r = np.random.default_rng(5)
+    c = np.concatenate([c, (r.normal(size=rep) + 1j * r.normal(size=rep))])
+    out = pl.sort_and_combine(soa(500, (x, z, f, c), cuda))
+    assert pl.sums.LAST_PLAN["key_words"] < 16
+    check_combined(out, R.combine(x, z, f, c))
+
+
+@pytest.mark.parametrize("m", [0, 1, 2, 33])
+def test_tiny_sums(cuda, m):
+    x, z, f, c = rng.c5_columns(max(m, 1), seed=3)
+    x, z, f, c = x[:m], z[:m], f[:m], c[:m]
+    out = pl.sort_and_combine(soa(500, (x, z, f, c), cuda))
+    if m == 0:
+        assert len(out) == 0
+    else:
+        check_combined(out, R.combine(x, z, f, c))
