@@ -36,6 +36,11 @@ WORKLOAD = ("C4: outer product + merge of two 10^4-term sums, n=500, weight 8 on
 L2_FLUSH_BYTES = 512 << 20
 
 
+# kernels launched under one stage-timer entry of the native library
+# (k_split: prep, count, bases, scatter; k_leaf_scan: the 3-kernel scan)
+KERNELS_PER_STAGE = {"k_split": 4, "k_leaf_scan": 3, "k_regroup": 3}
+
+
 def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -367,7 +372,8 @@ def main():
                        "l2": "512 MiB buffer written between timed steps; working set >> L2",
                        "key_words": kw, "buckets": plan.get("n_buckets")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": len(stages), "clocks": clk.summary(), "stage_share": stage_share,
+            "gpu_launches": sum(KERNELS_PER_STAGE.get(nm, 1) for nm, _ in stages),
+            "clocks": clk.summary(), "stage_share": stage_share,
             "secondary": secondary,
         }
         print(json.dumps(line), flush=True)

@@ -1338,8 +1338,11 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const O
     k_sample<W, KW, MODE><<<1, kLeafThreads, sm1, st>>>(L, D, S, C);
     PLB_CHECK_LAUNCH("k_sample");
   }
-  k_l1_table<KW><<<((1 << kTabBits) + 256) / 256, 256, 0, st>>>(D, C);
-  PLB_CHECK_LAUNCH("k_l1_table");
+  {
+    StageTimer t_(st, "k_l1_table");
+    k_l1_table<KW><<<((1 << kTabBits) + 256) / 256, 256, 0, st>>>(D, C);
+    PLB_CHECK_LAUNCH("k_l1_table");
+  }
   const size_t gsm = gen_smem_bytes(W, KW, D.nb1);
   dim3 ggrid;
   if (MODE == 0) ggrid = dim3((unsigned)ceil_div(D.ma, kGenThreads), (unsigned)ceil_div(D.mb, kGenTB));
@@ -1471,8 +1474,11 @@ static int run_partition(const pl_merge_plan& P, const SrcA& S, int64_t j0, int6
       k_sample<W, KW, 0><<<1, kLeafThreads, sm1, st>>>(L, D, S, C);
       PLB_CHECK_LAUNCH("k_sample");
     }
-    k_l1_table<KW><<<((1 << kTabBits) + 256) / 256, 256, 0, st>>>(D, C);
-    PLB_CHECK_LAUNCH("k_l1_table");
+    {
+      StageTimer t_(st, "k_l1_table");
+      k_l1_table<KW><<<((1 << kTabBits) + 256) / 256, 256, 0, st>>>(D, C);
+      PLB_CHECK_LAUNCH("k_l1_table");
+    }
     const size_t gsm = gen_smem_bytes(W, KW, D.nb1);
     const dim3 ggrid((unsigned)ceil_div(D.ma, kGenThreads), (unsigned)ceil_div(D.mb, kGenTB));
     if (D.nb1 > 1) {

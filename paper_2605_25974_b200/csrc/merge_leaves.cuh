@@ -763,8 +763,11 @@ static int launch_leaves(const Layout& L, const Dims& D, const SrcA& S, const Ct
     int rc = exclusive_scan_u32(C.kept, C.kprefix, D.max_leaves, C.scan_scratch, C.scan_total, st);
     if (rc) return rc;
   }
-  k_range_map<KW><<<(unsigned)ceil_div(D.max_leaves, 256), 256, 0, st>>>(D, C);
-  PLB_CHECK_LAUNCH("k_range_map");
+  {
+    StageTimer t_(st, "k_range_map");
+    k_range_map<KW><<<(unsigned)ceil_div(D.max_leaves, 256), 256, 0, st>>>(D, C);
+    PLB_CHECK_LAUNCH("k_range_map");
+  }
   const size_t esm = emit_smem_bytes(KW);
   auto ke = k_emit<W, KW>;
   if (esm > 48 * 1024)
