@@ -149,12 +149,30 @@ def group_greedy_parallel(s, chunks: int, *, stats: GroupingStats | None = None
     pieces = [p for p in np.array_split(np.arange(m), chunks) if p.size]
     locals_: list[list[int]] = []
     checks = 0
-    for p in pieces:
+
+    # phase 1: the chunks are independent, so each runs K6 on its own CUDA
+    # stream from its own host thread (the native call releases the GIL), as
+    # the reference runs them on a thread pool (grouping.py:118-124)
+    def run_chunk(p):
         r0, r1 = int(p[0]), int(p[-1]) + 1
-        gof, pc = _greedy_chunk(S, r0, r1, dev)
-        part = CommutationPartition.from_assignment(gof.cpu().numpy())
+        with torch.cuda.device(dev):
+            s = torch.cuda.Stream(dev)
+            s.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(s):
+                gof, pc = _greedy_chunk(S, r0, r1, dev)
+                return r0, gof.cpu().numpy(), int(pc.item())
+
+    if len(pieces) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=len(pieces)) as pool:
+            results = list(pool.map(run_chunk, pieces))
+    else:
+        results = [run_chunk(p) for p in pieces]
+    for r0, gof, pc in results:
+        part = CommutationPartition.from_assignment(gof)
         locals_.extend([[r0 + t for t in g] for g in part.groups])
-        checks += int(pc.item())
+        checks += pc
     n_local = len(locals_)
     if n_local == 0:
         if stats is not None:
