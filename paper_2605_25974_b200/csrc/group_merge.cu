@@ -13,9 +13,10 @@
 //                 anti-commuting pair marks the term's global group for this
 //                 epoch (anti_epoch[g] = epoch); a group already marked is
 //                 skipped.
-//   k_merge_pick  one CTA: first unmarked group in creation order (or a new
-//                 one), the pair_checks contribution (|L| * sizes of the groups
-//                 tried), L's members joined to it.
+//   pick          the last CTA of k_merge_anti to finish (completion counter):
+//                 first unmarked group in creation order (or a new one), the
+//                 pair_checks contribution (|L| * sizes of the groups tried),
+//                 L's members joined to it -- one launch per local group.
 #include "common.cuh"
 
 namespace plb {
@@ -24,11 +25,52 @@ constexpr int kMergeThreads = 256;
 // L members per shared-memory tile (<= 16 KB of x/z words)
 __host__ __device__ constexpr int merge_tile(int W) { return W >= 8 ? 1024 / W : 256; }
 
+// first unmarked global group (or a new one) for local group `epoch`, the
+// pair_checks contribution, and the members joined to it (one CTA)
+__device__ void merge_pick(int32_t* __restrict__ gid, const int32_t* __restrict__ members,
+                           int64_t lo, int64_t hi, int32_t epoch,
+                           const int32_t* __restrict__ anti_epoch, int32_t* __restrict__ gsize,
+                           int32_t* __restrict__ n_global, int32_t* __restrict__ global_of_local,
+                           int64_t* __restrict__ pair_checks) {
+  __shared__ int32_t s_first;
+  __shared__ unsigned long long s_tried;
+  const int32_t G = *(volatile int32_t*)n_global;
+  if (threadIdx.x == 0) {
+    s_first = G;
+    s_tried = 0;
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < G; g += blockDim.x)
+    if (((volatile const int32_t*)anti_epoch)[g] != epoch) atomicMin(&s_first, g);
+  __syncthreads();
+  const int32_t first = s_first;
+  // groups tried: 0..first (inclusive) when one fits, all G otherwise
+  const int32_t last = first < G ? first : G - 1;
+  unsigned long long part = 0;
+  for (int g = threadIdx.x; g <= last; g += blockDim.x) part += (unsigned long long)gsize[g];
+  if (part) atomicAdd(&s_tried, part);
+  __syncthreads();
+  const int64_t L = hi - lo;
+  if (threadIdx.x == 0) {
+    *pair_checks += (int64_t)s_tried * L;
+    if (first == G) {
+      gsize[G] = 0;
+      *n_global = G + 1;
+    }
+    gsize[first] += (int32_t)L;
+    global_of_local[epoch] = first;
+  }
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) gid[members[i]] = first;
+}
+
 template <int W>
 __global__ void __launch_bounds__(kMergeThreads)
 k_merge_anti(const u64* __restrict__ x, const u64* __restrict__ z, int64_t ld, int64_t M,
-             const int32_t* __restrict__ gid, const int32_t* __restrict__ members, int64_t lo,
-             int64_t hi, int32_t epoch, int32_t* __restrict__ anti_epoch) {
+             int32_t* __restrict__ gid, const int32_t* __restrict__ members, int64_t lo,
+             int64_t hi, int32_t epoch, int32_t* __restrict__ anti_epoch,
+             int32_t* __restrict__ gsize, int32_t* __restrict__ n_global,
+             int32_t* __restrict__ global_of_local, int64_t* __restrict__ pair_checks,
+             unsigned int* __restrict__ done) {
   constexpr int kMergeTile = merge_tile(W);
   __shared__ u64 lx[W][kMergeTile], lz[W][kMergeTile];
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -67,6 +109,17 @@ k_merge_anti(const u64* __restrict__ x, const u64* __restrict__ z, int64_t ld, i
       }
     }
   }
+  // the last CTA to finish picks (no second launch per local group)
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  merge_pick(gid, members, lo, hi, epoch, anti_epoch, gsize, n_global, global_of_local,
+             pair_checks);
+  if (threadIdx.x == 0) *done = 0u;  // ready for the next local group
 }
 
 __global__ void __launch_bounds__(1024)
@@ -74,35 +127,8 @@ k_merge_pick(int32_t* __restrict__ gid, const int32_t* __restrict__ members, int
              int64_t hi, int32_t epoch, const int32_t* __restrict__ anti_epoch,
              int32_t* __restrict__ gsize, int32_t* __restrict__ n_global,
              int32_t* __restrict__ global_of_local, int64_t* __restrict__ pair_checks) {
-  __shared__ int32_t s_first;
-  __shared__ unsigned long long s_tried;
-  const int32_t G = *n_global;
-  if (threadIdx.x == 0) {
-    s_first = G;
-    s_tried = 0;
-  }
-  __syncthreads();
-  for (int g = threadIdx.x; g < G; g += blockDim.x)
-    if (anti_epoch[g] != epoch) atomicMin(&s_first, g);
-  __syncthreads();
-  const int32_t first = s_first;
-  // groups tried: 0..first (inclusive) when one fits, all G otherwise
-  const int32_t last = first < G ? first : G - 1;
-  unsigned long long part = 0;
-  for (int g = threadIdx.x; g <= last; g += blockDim.x) part += (unsigned long long)gsize[g];
-  if (part) atomicAdd(&s_tried, part);
-  __syncthreads();
-  const int64_t L = hi - lo;
-  if (threadIdx.x == 0) {
-    *pair_checks += (int64_t)s_tried * L;
-    if (first == G) {
-      gsize[G] = 0;
-      *n_global = G + 1;
-    }
-    gsize[first] += (int32_t)L;
-    global_of_local[epoch] = first;
-  }
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) gid[members[i]] = first;
+  merge_pick(gid, members, lo, hi, epoch, anti_epoch, gsize, n_global, global_of_local,
+             pair_checks);
 }
 
 template <int W>
@@ -112,18 +138,22 @@ static int run_merge(int64_t M, const u64* x, const u64* z, int64_t ld, const in
   int32_t* gid = (int32_t*)ws;
   int32_t* anti_epoch = gid + M;
   int32_t* gsize = anti_epoch + n_local;
+  unsigned int* done = (unsigned int*)(gsize + n_local);
   PLB_CUDA(cudaMemsetAsync(gid, 0xFF, 4 * (size_t)M, st));           // -1: not placed yet
   PLB_CUDA(cudaMemsetAsync(anti_epoch, 0xFF, 4 * (size_t)n_local, st));
   PLB_CUDA(cudaMemsetAsync(n_global, 0, 4, st));
+  PLB_CUDA(cudaMemsetAsync(done, 0, 4, st));
   const unsigned grid = (unsigned)ceil_div(M, kMergeThreads);
   StageTimer t_(st, "k_group_merge");
   for (int32_t l = 0; l < n_local; ++l) {
     const int64_t lo = local_off[l], hi = local_off[l + 1];
-    if (l > 0)
+    if (l > 0)  // marks, then its last CTA picks
       k_merge_anti<W><<<grid, kMergeThreads, 0, st>>>(x, z, ld, M, gid, members, lo, hi, l,
-                                                      anti_epoch);
-    k_merge_pick<<<1, 1024, 0, st>>>(gid, members, lo, hi, l, anti_epoch, gsize, n_global,
-                                      global_of_local, pair_checks);
+                                                      anti_epoch, gsize, n_global,
+                                                      global_of_local, pair_checks, done);
+    else
+      k_merge_pick<<<1, 1024, 0, st>>>(gid, members, lo, hi, l, anti_epoch, gsize, n_global,
+                                        global_of_local, pair_checks);
   }
   PLB_CHECK_LAUNCH("k_group_merge");
   return PL_OK;
@@ -134,7 +164,7 @@ static int run_merge(int64_t M, const u64* x, const u64* z, int64_t ld, const in
 using namespace plb;
 
 extern "C" int64_t pl_group_merge_workspace_bytes(int64_t M, int32_t n_local) {
-  return 4 * (M + 2 * (int64_t)n_local + 64);
+  return 4 * (M + 2 * (int64_t)n_local + 64);  // gid | anti_epoch | gsize | done
 }
 
 extern "C" int pl_group_merge(int W, int64_t M, const uint64_t* x, const uint64_t* z, int64_t ld,
