@@ -46,7 +46,7 @@ namespace plb {
 
 constexpr int kGenThreads = 256;
 constexpr int kGenTB = 16;        // b-terms per tile (outer) / terms per thread (sort)
-constexpr int kLeafThreads = 512;
+constexpr int kLeafThreads = 1024;  // k_sample (one-CTA sample sort)
 constexpr int kSplitThreads = 1024;
 constexpr int kSortSmemBytes = 200 * 1024;
 constexpr int kSampleOversample = 16;  // level-2 samples per sub-bucket
@@ -462,8 +462,16 @@ k_sample(Layout L, Dims D, SrcA S, Ctl C) {
   for (int s = threadIdx.x; s < ns; s += blockDim.x) {
     const int64_t r = ((2 * (int64_t)s + 1) * D.n_space) / (2 * (int64_t)ns);
     u64 key[KW];
-    int k;
-    Source<W, KW, MODE>::item_at(L, S, D.ma, r, key, k);
+    // packed keys of the operands are already in C.opk (k_pack_ops)
+    if (MODE == 1) {
+#pragma unroll
+      for (int d = 0; d < KW; ++d) key[d] = C.opk[d * D.ma + r];
+    } else {
+      const int64_t nops = D.ma + D.mb_all;
+      const int64_t j = r / D.ma, i = r - j * D.ma;
+#pragma unroll
+      for (int d = 0; d < KW; ++d) key[d] = C.opk[d * nops + i] ^ C.opk[d * nops + D.ma + j];
+    }
     store_key<KW>(K, ns, s, key);
     I[s] = (uint32_t)s;
   }
