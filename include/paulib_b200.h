@@ -67,8 +67,9 @@ int pl_batch_sip(int W, int64_t P,
  * K2 raw — outer product without combine.  Replaces sums.py:144-174
  * (_multiply_columns) + sums.py:123-141 (_multiply_block): output row
  * j*Ma + i holds a_i * b_j (j-major), phase exponent
- * (a.k[i] + b.k[j] + phase(a_i, b_j)) mod 4 and coefficient a.c[i] * b.c[j]
- * (IEEE products, no fused multiply-add).  Output planes have Ma*Mb columns.
+ * (a.k[i] + b.k[j] + phase(a_i, b_j)) mod 4 and coefficient a.c[i] * b.c[j],
+ * rounded as numpy's complex128 multiply on FMA hosts: re = fma(ar, br, -(ai*bi)),
+ * im = fma(ar, bi, ai*br).  Output planes have Ma*Mb columns.
  */
 int pl_outer_multiply_raw(int W, int64_t Ma, int64_t Mb,
                           const uint64_t* ax, const uint64_t* az, const uint8_t* ak,
@@ -118,7 +119,8 @@ int pl_sort_plan(int W, int64_t M, const uint64_t* x, const uint64_t* z, int64_t
 
 /* Outer product followed by _combine_columns (sums.py:94-120): fold i^k into
  * the coefficient, order by the canonical key, merge equal keys (summing in
- * raw-row order), drop |c| <= eps, flags 0.  Output planes need capacity
+ * raw-row order), drop |c| <= eps (any eps, as _combine_columns: a negative
+ * eps keeps every merged term, exact zeros included), flags 0.  Output planes need capacity
  * >= plan->n_items columns (ldo); *out_count (device int64) receives the
  * number of merged terms.  Deterministic: bit-identical run to run. */
 int pl_outer_multiply_combine(const pl_merge_plan* plan,

@@ -84,7 +84,7 @@ extern "C" int pl_outer_multiply_combine(const pl_merge_plan* plan, const uint64
                                          int64_t ldo, int64_t* out_count, void* stream) {
   int rc = check_ws(plan, workspace, workspace_bytes, 0);
   if (rc) return rc;
-  if (eps < 0 || ldo < plan->n_items || !out_count) {
+  if (eps != eps || ldo < plan->n_items || !out_count) {
     set_error("pl_outer_multiply_combine: bad arguments");
     return PL_ERR_ARG;
   }
@@ -106,7 +106,7 @@ extern "C" int pl_sort_combine(const pl_merge_plan* plan, const uint64_t* x, con
                                int64_t* out_count, void* stream) {
   int rc = check_ws(plan, workspace, workspace_bytes, 1);
   if (rc) return rc;
-  if (eps < 0 || ldo < plan->n_items || !out_count) {
+  if (eps != eps || ldo < plan->n_items || !out_count) {
     set_error("pl_sort_combine: bad arguments");
     return PL_ERR_ARG;
   }
@@ -163,7 +163,7 @@ extern "C" int pl_merge_received(const pl_merge_plan* plan, const void* recv, in
                                  uint64_t* ox, uint64_t* oz, uint8_t* ok, double* oc, int64_t ldo,
                                  int64_t* out_count, void* stream) {
   if (!plan || plan->mode != 0 || n_ranks < 1 || n_ranks > 64 || b0 < 0 || b1 <= b0 ||
-      b1 > plan->n_buckets || n_recv < 0 || ldo < n_recv || eps < 0 || !out_count) {
+      b1 > plan->n_buckets || n_recv < 0 || ldo < n_recv || eps != eps || !out_count) {
     set_error("pl_merge_received: bad arguments");
     return PL_ERR_ARG;
   }

@@ -28,7 +28,7 @@ import torch.distributed as dist
 
 from . import _native
 from ._device import cuda_device, ptr, stream_ptr
-from .sums import PauliSumSoA, _alloc_planes, _download, _new_sum, _remember
+from .sums import PauliSumSoA, _alloc_planes, _download, _fitted, _new_sum, _remember
 
 
 def block_range(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -50,19 +50,25 @@ def exchange(send: torch.Tensor, bucket_counts: torch.Tensor, item_bytes: int, g
     nb = bucket_counts.numel()
     if world == 1:
         return send, bucket_counts.view(1, nb), 0, nb
-    gathered = [torch.empty_like(bucket_counts) for _ in range(world)]
-    dist.all_gather(gathered, bucket_counts, group=group)
+    home = send.device
+    # gloo moves host tensors only: device records are staged through host
+    # memory (the multi-process tests on one GPU); NCCL moves device memory
+    staged = home.type == "cuda" and dist.get_backend(group) == "gloo"
+    wire = torch.device("cpu") if staged else home
+    counts = bucket_counts.to(wire)
+    gathered = [torch.empty_like(counts) for _ in range(world)]
+    dist.all_gather(gathered, counts, group=group)
     cm = torch.stack(gathered).to("cpu", torch.int64).numpy()  # (G, nb)
     ranges = [block_range(nb, world, q) for q in range(world)]
     b0, b1 = ranges[rank]
     send_split = [int(cm[rank, lo:hi].sum()) * item_bytes for lo, hi in ranges]
     recv_split = [int(cm[s, b0:b1].sum()) * item_bytes for s in range(world)]
-    recv = torch.empty(max(sum(recv_split), 1), dtype=torch.uint8, device=send.device)
+    recv = torch.empty(max(sum(recv_split), 1), dtype=torch.uint8, device=wire)
     recv_view = recv[:sum(recv_split)]
-    send_view = send[:sum(send_split)]
+    send_view = send[:sum(send_split)].to(wire)
     dist.all_to_all_single(recv_view, send_view, recv_split, send_split, group=group)
-    local = torch.from_numpy(np.ascontiguousarray(cm[:, b0:b1]).astype(np.int32)).to(send.device)
-    return recv_view, local, b0, b1
+    local = torch.from_numpy(np.ascontiguousarray(cm[:, b0:b1]).astype(np.int32)).to(home)
+    return recv_view.to(home), local, b0, b1
 
 
 def partition(A, B, plan, j0: int, j1: int, dev):
@@ -98,8 +104,7 @@ def merge_received(A, B, plan, recv, counts, b0: int, b1: int, eps: float, dev, 
                      ptr(A.x), ptr(A.z), ptr(A.k), ptr(A.c), A.ld,
                      ptr(B.x), ptr(B.z), ptr(B.k), ptr(B.c), B.ld, float(eps), ptr(ws), ws.numel(),
                      ptr(x), ptr(z), ptr(k), ptr(c), x.stride(0), ptr(cnt), stream_ptr(dev))
-    m = int(cnt.item())
-    return _new_sum(n, x[:, :m], z[:, :m], k[:m], c[:m])
+    return _fitted(n, x, z, k, c, int(cnt.item()))
 
 
 def _plan(A, B, dev):
@@ -117,8 +122,6 @@ def sharded_outer_multiply(a: PauliSumSoA, b: PauliSumSoA, *, group=None, eps: f
 
     A and B are replicated on every rank.  Host inputs are uploaded and the
     shard is returned to host memory (end-to-end path)."""
-    if eps < 0:
-        raise ValueError("eps must be >= 0")
     a._check_same_n(b)
     back = a.device.type != "cuda" and b.device.type != "cuda"
     dev = cuda_device(device if device is not None else (a.device if not back else None))
@@ -133,7 +136,10 @@ def sharded_outer_multiply(a: PauliSumSoA, b: PauliSumSoA, *, group=None, eps: f
     j0, j1 = block_range(B.M, world, rank)
     send, counts, item = partition(A, B, plan, j0, j1, dev)
     recv, cm, b0, b1 = exchange(send, counts, item, group)
-    out = merge_received(A, B, plan, recv, cm, b0, b1, eps, dev, a.n)
+    if b1 > b0:
+        out = merge_received(A, B, plan, recv, cm, b0, b1, eps, dev, a.n)
+    else:  # fewer buckets than ranks: this rank owns no key range (still joined the exchange)
+        out = PauliSumSoA.empty(a.n, device=dev)
     return _download(out) if back else out
 
 

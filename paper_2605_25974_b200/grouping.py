@@ -99,6 +99,7 @@ def group_assignment(s: PauliSumSoA):
 
 
 _PL_ERR_WORKSPACE = -5
+_MAX_CHUNK_STREAMS = 8
 
 
 def group_greedy(s, *, stats: GroupingStats | None = None) -> CommutationPartition:
@@ -165,7 +166,9 @@ def group_greedy_parallel(s, chunks: int, *, stats: GroupingStats | None = None
     if len(pieces) > 1:
         from concurrent.futures import ThreadPoolExecutor
 
-        with ThreadPoolExecutor(max_workers=len(pieces)) as pool:
+        # at most _MAX_CHUNK_STREAMS chunks in flight: bounded host threads,
+        # streams and concurrently allocated K6 workspaces for any chunk count
+        with ThreadPoolExecutor(max_workers=min(len(pieces), _MAX_CHUNK_STREAMS)) as pool:
             results = list(pool.map(run_chunk, pieces))
     else:
         results = [run_chunk(p) for p in pieces]

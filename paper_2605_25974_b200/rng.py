@@ -144,13 +144,25 @@ def random_columns(n: int, m: int, seed: int):
     return x, z, np.zeros(m, np.uint8), coeffs
 
 
-def random_sum(n: int, m: int, seed: int, *, layout: str = "soa"):
-    """Uniform random sum, identical draws to the reference ``random_sum``."""
+def random_sum(n: int, m: int, seed: int, *, layout: str = "aos"):
+    """Uniform random sum, identical draws to the reference ``random_sum``
+    (rng.py:73-82).  Returns the reference's packed ``PauliSum`` by default;
+    ``layout="soa"`` gives device-ready ``PauliSumSoA`` planes instead."""
     from .sums import PauliSum, PauliSumSoA
 
     cols = random_columns(n, m, seed)
     cls = PauliSumSoA if layout == "soa" else PauliSum
     return cls.from_columns(n, *cols)
+
+
+def random_string(n: int, stream: SplitMix64):
+    """One uniform string, phase 0 (rng.py:66-70): consumes exactly n draws of
+    ``stream`` (letter code = draw & 3, 0=I 1=X 2=Y 3=Z)."""
+    from .strings import PauliString
+
+    codes = (stream.next_array(n) & _U64(3)).astype(np.uint8)[None, :]
+    x, z = _letter_codes_to_words(codes, n)
+    return PauliString(n, x[0], z[0], 0, validate=False)
 
 
 def local_columns(n: int, m: int, stream: SplitMix64, universe: int, weight,

@@ -99,6 +99,25 @@ class PauliString:
     def weight(self) -> int:
         return int(np.bitwise_count(self.x | self.z).sum())
 
+    def apply_clifford(self, gate: str, qubits) -> "PauliString":
+        """U * self * U^dagger for a Clifford gate (strings.py:153-163); a new
+        string.  Runs the f2 kernel (``pl_apply_clifford``) on a one-term sum."""
+        from . import gates
+
+        if isinstance(qubits, (int, np.integer)):
+            qubits = (int(qubits),)
+        else:
+            qubits = tuple(int(q) for q in qubits)
+        code, q0, q1 = gates.check_gate(gate, qubits, self.n)
+        dev = cuda_device()
+        x = _dev_planes(self.x, dev)
+        z = _dev_planes(self.z, dev)
+        k = torch.tensor([self.phase], dtype=torch.uint8, device=dev)
+        with torch.cuda.device(dev):
+            gates.apply_clifford_planes(x, z, k, 1, self.words, 1, code, q0, q1, dev)
+        return PauliString(self.n, i64_tensor_to_u64(x)[:, 0], i64_tensor_to_u64(z)[:, 0],
+                           int(k.item()), validate=False)
+
     def canonical_key(self) -> bytes:
         """(z words, x words) big-endian, phase ignored (strings.py:165-167)."""
         return self.z.astype(">u8").tobytes() + self.x.astype(">u8").tobytes()
@@ -224,3 +243,8 @@ def ps_commutes(a: PauliString, b: PauliString) -> bool:
 
 def ps_weight(p: PauliString) -> int:
     return p.weight()
+
+
+def ps_apply_clifford(p: PauliString, gate: str, qubits) -> PauliString:
+    """strings.py:215-216."""
+    return p.apply_clifford(gate, qubits)

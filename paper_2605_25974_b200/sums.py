@@ -294,8 +294,6 @@ class PauliSumSoA:
         from .rotations import check_rotation_n, rotation_split
 
         check_rotation_n(self.n, rot)
-        if eps < 0:
-            raise ValueError("eps must be >= 0")
         dev, back = _compute_device(self)
         with torch.cuda.device(dev):
             if len(self) == 0:
@@ -492,6 +490,17 @@ def _new_sum(n, x, z, k, c) -> PauliSumSoA:
     return out
 
 
+def _fitted(n, x, z, k, c, m: int) -> PauliSumSoA:
+    """The first m merged terms of capacity-sized output planes.  Views are
+    kept while they waste at most half the allocation; a heavily merged
+    result (e.g. H*H) is copied into right-sized tensors so the raw-size
+    buffers are released instead of staying alive with the result."""
+    cap = x.shape[1]
+    if 2 * m >= cap:
+        return _new_sum(n, x[:, :m], z[:, :m], k[:m], c[:m])
+    return _new_sum(n, x[:, :m].clone(), z[:, :m].clone(), k[:m].clone(), c[:m].clone())
+
+
 def _alloc_planes(W: int, cap: int, dev):
     x = torch.empty((W, max(cap, 1)), dtype=torch.int64, device=dev)
     z = torch.empty((W, max(cap, 1)), dtype=torch.int64, device=dev)
@@ -502,9 +511,10 @@ def _alloc_planes(W: int, cap: int, dev):
 
 def outer_multiply(a: PauliSumSoA, b: PauliSumSoA, *, eps: float = 0.0, combine: bool = True):
     """A*B on the GPU: raw j-major product (sums.py:144-174) or combined
-    (sums.py:94-120).  Returns a PauliSumSoA on A's device (host in -> host out)."""
-    if eps < 0:
-        raise ValueError("eps must be >= 0")
+    (sums.py:94-120).  Returns a PauliSumSoA on A's device (host in -> host out).
+
+    Like the reference's multiply, any ``eps`` is accepted: a negative one
+    keeps every merged term, exact zeros included (sums.py:113-114)."""
     dev, back = _compute_device(a, b)
     A = a.to(dev).planes()
     B = b.to(dev).planes()
@@ -534,15 +544,14 @@ def outer_multiply(a: PauliSumSoA, b: PauliSumSoA, *, eps: float = 0.0, combine:
                          ptr(B.x), ptr(B.z), ptr(B.k), ptr(B.c), B.ld,
                          float(eps), ptr(ws), ws.numel(),
                          ptr(x), ptr(z), ptr(k), ptr(c), x.stride(0), ptr(cnt), st)
-            m = int(cnt.item())
-            out = _new_sum(a.n, x[:, :m], z[:, :m], k[:m], c[:m])
+            out = _fitted(a.n, x, z, k, c, int(cnt.item()))
     return _download(out) if back else out
 
 
 def sort_combine(s: PauliSumSoA, *, eps: float = 0.0) -> PauliSumSoA:
-    """sort_and_combine on the GPU (sums.py:94-120, :286-291)."""
-    if eps < 0:
-        raise ValueError("eps must be >= 0")
+    """_combine_columns on the GPU (sums.py:94-120).  The public
+    sort_and_combine rejects eps < 0 (sums.py:288-289); this internal entry
+    (also used by apply_rotation) accepts any eps like _combine_columns."""
     dev, back = _compute_device(s)
     S = s.to(dev).planes()
     W, m = S.W, S.M
@@ -560,8 +569,7 @@ def sort_combine(s: PauliSumSoA, *, eps: float = 0.0) -> PauliSumSoA:
             _native.call("pl_sort_combine", C.byref(plan), ptr(S.x), ptr(S.z), ptr(S.k),
                          ptr(S.c), S.ld, float(eps), ptr(ws), ws.numel(),
                          ptr(x), ptr(z), ptr(k), ptr(c), x.stride(0), ptr(cnt), st)
-            mm = int(cnt.item())
-            out = _new_sum(s.n, x[:, :mm], z[:, :mm], k[:mm], c[:mm])
+            out = _fitted(s.n, x, z, k, c, int(cnt.item()))
     return _download(out) if back else out
 
 
@@ -578,6 +586,16 @@ def sort_and_combine(s, eps: float = 0.0):
 def sum_multiply(a, b, *, threads: int = 1, eps: float = 0.0, combine: bool = True):
     """sums.py:488-489."""
     return a.multiply(b, threads=threads, eps=eps, combine=combine)
+
+
+def sum_apply_clifford(s, gate: str, qubits) -> None:
+    """sums.py:492-493: conjugate every term of ``s`` in place."""
+    s.apply_clifford(gate, qubits)
+
+
+def sum_apply_rotation(s, rot, *, eps: float = 0.0, combine: bool = True):
+    """sums.py:496-497."""
+    return s.apply_rotation(rot, eps=eps, combine=combine)
 
 
 def to_soa(s: PauliSum, device=None) -> PauliSumSoA:
