@@ -115,26 +115,62 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU side
-def cpu_outer_sample(a, b, m: int, threads: int, repeats: int = 2):
-    """Time the oracle restatement of sum_multiply (sums.py:293-305) on the
-    first m x m terms; returns (pair-products/s, seconds per run)."""
+CPU_SAMPLE_M = 3163          # 3163 x 3163 ~ 10^7 pair products per CPU step
+C4_PRODUCTS = 10_000 * 10_000
+
+
+def nlogn_scale(n_sample: int, n_full: int) -> float:
+    """Time ratio T(n_full) / T(n_sample) for an n log n sort-and-merge
+    (the CPU C4 baseline is timed at ~10^7 and extrapolated)."""
+    import math
+
+    return (n_full * math.log(n_full)) / (n_sample * math.log(n_sample))
+
+
+def host_info() -> dict:
+    info = {"cpu_count": os.cpu_count(), "affinity": None, "cpu_model": None, "ram_gb": None}
+    try:
+        info["affinity"] = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        pass
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                info["ram_gb"] = round(int(line.split()[1]) / 2**20, 1)
+                break
+    except OSError:
+        pass
+    return info
+
+
+def cpu_outer_time(A, B, threads: int) -> float:
+    """Seconds for the oracle restatement of sum_multiply (sums.py:293-305):
+    multiply threaded over j-blocks (sums.py:158-173), combine single-threaded
+    (sums.py:94-120), on the given prefix operands."""
     from oracle import numpy_ref as R
 
-    A = tuple(x[:m] for x in a)
-    B = tuple(x[:m] for x in b)
-    R.outer_combine(*A, *B, threads=threads)  # warm-up
-    best = None
-    for _ in range(repeats):
-        t0 = time.perf_counter()
-        R.outer_combine(*A, *B, threads=threads)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    return m * m / best, best
+    t0 = time.perf_counter()
+    R.outer_combine(*A, *B, threads=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_sample_desc(m: int, threads: int) -> str:
+    return (f"first {m} x {m} terms of the C4 inputs ({m * m} pair products) per step, time "
+            f"extrapolated to the full 10^8 products as n log n (x{nlogn_scale(m * m, C4_PRODUCTS):.3f}, "
+            f"BASELINE.md §3); multiply threaded over {threads} threads (sums.py:158-173), "
+            f"combine single-threaded (sums.py:94-120)")
 
 
 def run_reference(args, rank: int, world: int):
     """--impl reference: the reference's CPU algorithm (numpy port in oracle/;
-    the reference is pure Python and cannot be compiled) on this host's cores."""
+    the reference is pure Python, nothing to compile) on this host's cores, on
+    the C4 workload: each timed step is a ~10^7-product prefix sample whose
+    time is extrapolated n log n to the 10^8-product step.  Warm-up steps use
+    a 10^6-product prefix."""
     if rank != 0:
         return
     from paper_2605_25974_b200 import rng
@@ -142,32 +178,72 @@ def run_reference(args, rank: int, world: int):
     a, b = rng.config_columns(4)
     threads = os.cpu_count() or 1
     m = args.cpu_sample
-    times = []
-    from oracle import numpy_ref as R
-
     A = tuple(x[:m] for x in a)
     B = tuple(x[:m] for x in b)
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        R.outer_combine(*A, *B, threads=threads)
-        dt = time.perf_counter() - t0
-        if i >= args.warmup:
-            times.append(dt)
+    for _ in range(args.warmup):
+        cpu_outer_time(tuple(x[:1000] for x in a), tuple(x[:1000] for x in b), threads)
+    scale = nlogn_scale(m * m, C4_PRODUCTS)
+    times = [cpu_outer_time(A, B, threads) * scale for _ in range(args.steps)]
     tot = sum(times)
-    value = m * m * len(times) / tot
-    sample = (f"first {m} x {m} terms of the C4 inputs ({m * m} pair products) per step; "
-              f"multiply threaded over {threads} threads like sums.py:158-173, combine single-threaded")
+    value = C4_PRODUCTS * len(times) / tot
+    sample = cpu_sample_desc(m, threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64+c128",
         "data": "synthetic (seeded SplitMix64 generator, DESIGN.md Inputs)",
-        "config": {"workload": WORKLOAD, "sampled": sample},
+        "config": {"workload": WORKLOAD, "pair_products_per_step": C4_PRODUCTS,
+                   "sampled": sample, "extrapolated": "n log n from the timed sample",
+                   "host": host_info()},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- launcher
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: re-run this command as N ranks
+    (one process per GPU) under torch.distributed.run on 127.0.0.1.  NCCL's
+    INIT log goes to per-process files so rank 0 can report the communicator
+    size NCCL itself saw."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", NCCL_LOG_PATTERN)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+NCCL_LOG_PATTERN = "/tmp/paulib_nccl.%h.%p.log"
+
+
+def nccl_nranks() -> int | None:
+    """nRanks of this process's NCCL communicator, from its INIT log (if any)."""
+    import re
+    import socket
+
+    pat = os.environ.get("NCCL_DEBUG_FILE")
+    if not pat:
+        return None
+    path = Path(pat.replace("%h", socket.gethostname()).replace("%p", str(os.getpid())))
+    try:
+        text = path.read_text(errors="replace")
+    except OSError:
+        return None
+    found = re.findall(r"nRanks (\d+)", text) or re.findall(r"nranks (\d+)", text)
+    return int(found[-1]) if found else None
 
 
 # --------------------------------------------------------------- GPU side
@@ -185,13 +261,28 @@ def main():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=1000)
+    ap.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE_M)
+    ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.launch_check:  # CPU test of the launcher: gloo rendezvous, no GPU work
+        import torch
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        t = torch.tensor([rank + 1])
+        dist.all_reduce(t)
+        if rank == 0:
+            print(json.dumps({"launch_check": True, "world": dist.get_world_size(),
+                              "rank_sum": int(t.item())}), flush=True)
+        dist.destroy_process_group()
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -350,16 +441,21 @@ def main():
     if world == 1 and rank == 0:
         if not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
-            v, sec = cpu_outer_sample(a_cols, b_cols, args.cpu_sample, threads)
-            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                   "sample": (f"first {args.cpu_sample} x {args.cpu_sample} terms of the C4 "
-                              f"inputs ({args.cpu_sample ** 2} pair products), min of 2 runs "
-                              f"({sec:.2f} s each); multiply threaded over {threads} threads, "
-                              f"combine single-threaded (sums.py:158-173, :94-120)")}
+            m = args.cpu_sample
+            sec = cpu_outer_time(tuple(x[:m] for x in a_cols), tuple(x[:m] for x in b_cols),
+                                 threads)
+            t_full = sec * nlogn_scale(m * m, C4_PRODUCTS)
+            cpu = {"value": C4_PRODUCTS / t_full, "unit": UNIT, "cores": threads, "kind": "port",
+                   "sample": cpu_sample_desc(m, threads) + f"; one run, {sec:.2f} s",
+                   "host": host_info()}
         if not args.no_secondary:
             from bench_secondary import run_secondary
 
             secondary = run_secondary(dev, flush)
+    elif world > 1 and not args.no_secondary:
+        from bench_secondary import c5_bitmatrix_sharded
+
+        secondary = c5_bitmatrix_sharded(dev, flush, group)
 
     if rank == 0:
         line = {
@@ -374,6 +470,7 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": sum(KERNELS_PER_STAGE.get(nm, 1) for nm, _ in stages),
             "clocks": clk.summary(), "stage_share": stage_share,
+            "nccl_nranks": nccl_nranks() if world > 1 else None,
             "secondary": secondary,
         }
         print(json.dumps(line), flush=True)

@@ -211,6 +211,42 @@ def f12(dev, flush):
     return out
 
 
+def c5_bitmatrix_sharded(dev, flush, group) -> dict:
+    """N>1: the C5 commutation bitmatrix row-sharded over the ranks (north
+    star: row blocks, inputs replicated, no collective).  Each rank computes
+    rows [r*M/G, (r+1)*M/G) in 65,536-row chunks; whole-job checks/s = M^2 /
+    the slowest rank's time."""
+    import torch.distributed as dist
+
+    from paper_2605_25974_b200 import dist as pdist
+
+    x, z, f, c = rng.c5_columns(1_000_000, seed=4)
+    S = pl.PauliSumSoA.from_columns(500, x, z, f, c, device=dev)
+    M = len(S)
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    r0, r1 = pdist.block_range(M, world, rank)
+    rows = 65536
+    nw = (M + 31) // 32
+    buf = torch.empty((rows, nw), dtype=torch.int32, device=dev)
+
+    def shard():
+        for q0 in range(r0, r1, rows):
+            r = min(rows, r1 - q0)
+            pl.commutation_bitmatrix(S, row0=q0, rows=r, out=buf[:r])
+
+    dist.barrier(group, device_ids=[dev.index])
+    ms = _timed(shard, dev, flush, 2, warm=1)
+    t = torch.tensor([statistics.mean(ms)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    t = float(t.item())
+    out_bytes = M * nw * 4
+    return {"c5_bitmatrix_sharded": {
+        "workload": f"C5 full commutation bitmatrix 10^6 x 10^6, row blocks over {world} GPUs",
+        "value": float(M) * M / (t / 1e3), "unit": "checks/s", "ms_per_step": t,
+        "scaling": "strong", "n_gpus": world, "output_bytes": out_bytes,
+        "timing": "CUDA events per rank, max over ranks"}}
+
+
 def run_secondary(dev, flush) -> dict:
     out = {}
     for fn in (c2, c1, c5, c3, f12, f3):

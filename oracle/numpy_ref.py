@@ -73,6 +73,21 @@ def outer_raw(ax, az, af, ac, bx, bz, bf, bc, threads: int = 1, chunk: int = 1 <
     return out_x, out_z, out_k, out_c
 
 
+def outer_raw_rows(ax, az, af, ac, bx, bz, bf, bc, rows):
+    """Selected rows r = j*Ma + i of the raw outer product (sums.py:123-141):
+    x = a_x ^ b_x, z = a_z ^ b_z, k = (base_a + base_b + 2popc(az&bx) -
+    popc(x&z)) mod 4 with base = flags + popc(x&z) (sums.py:156-157), coeff
+    a_c[i]*b_c[j].  Rows come out in the given order."""
+    ma = ax.shape[0]
+    rows = np.asarray(rows, dtype=np.int64)
+    j, i = np.divmod(rows, ma)
+    axs, azs, bxs, bzs = ax[i], az[i], bx[j], bz[j]
+    x, z = axs ^ bxs, azs ^ bzs
+    k = (af[i].astype(np.int64) + _pc(axs & azs) + bf[j].astype(np.int64) + _pc(bxs & bzs)
+         + 2 * _pc(azs & bxs) - _pc(x & z))
+    return x, z, np.mod(k, 4).astype(np.uint8), ac[i] * bc[j]
+
+
 def canonical_order(x, z) -> np.ndarray:
     """Stable permutation sorting rows by (z_0..z_{W-1}, x_0..x_{W-1}) as unsigned
     words, z_0 most significant (sums.py:104-106, strings.py:165-167)."""

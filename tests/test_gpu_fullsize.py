@@ -1,0 +1,142 @@
+"""GPU parity on the exact benchmarked inputs (BASELINE configs 4 and 5 at
+full size), checked against the oracle with bounded host memory:
+
+* C4, 10^8 pair products (sums.py:94-174): the GPU output's key space is cut
+  into ranges at its own row quantiles; one host pass over all raw products
+  (j-major chunks, exactly the reference's raw-row order) assigns every raw
+  row to its range; each range is then restated by the oracle (raw rows ->
+  combine) and compared with the matching slice of the GPU output.  Together
+  the ranges cover every output term.  Plus device-side properties of the whole
+  output: strictly increasing canonical keys, phases 0, no exact zeros.
+* C5 simplify, 10^6 terms (sums.py:484): the whole output against oracle.combine.
+* C5 commutation bitmatrix (grouping.py:136-140): 64-row windows at several
+  offsets of the 65,536-row chunks the bench computes, all 10^6 columns.
+* C5 greedy grouping (grouping.py:67-95): the full 10^6-term run; first-fit is
+  prefix-closed, so its first 20,000 assignments must equal the C oracle's on
+  the 20,000-term prefix, and so must the GPU run on the prefix alone.
+"""
+
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2605_25974_b200 as pl
+from paper_2605_25974_b200 import rng
+from oracle import numpy_ref as R
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+TOL = 1e-12  # north_star: merged coefficients within 1e-12 of the summed magnitudes
+
+
+def soa(n, cols, dev):
+    return pl.PauliSumSoA.from_columns(n, *cols, device=dev)
+
+
+def test_c4_full_parity_by_key_ranges(cuda):
+    a, b = rng.config_columns(4)
+    A, B = soa(500, a, cuda), soa(500, b, cuda)
+    ma, mb = len(A), len(B)
+    out = pl.outer_multiply(A, B)
+    m = len(out)
+    assert 0 < m <= ma * mb
+
+    # C4 keys live in word 0 (qubits 0..47): the canonical order is (z0, x0)
+    for v in (a[0], a[1], b[0], b[1]):
+        assert not v[:, 1:].any() and not (v[:, 0] >> np.uint64(48)).any()
+    assert not out.x[1:].any() and not out.z[1:].any()
+    assert not out.flags.any()
+    assert bool((torch.view_as_real(out.coeffs) != 0).any(dim=1).all())
+    z0, x0 = out.z[0], out.x[0]  # < 2^48: int64 order == unsigned order
+    dz = z0[1:] - z0[:-1]
+    assert bool((dz >= 0).all())
+    assert bool(((dz > 0) | (x0[1:] > x0[:-1])).all())  # strictly increasing keys
+
+    # key ranges [zb[r], zb[r+1]) on z0 at the output's row quantiles
+    nr = 48
+    picks = torch.tensor([r * m // nr for r in range(1, nr)], device=cuda)
+    zb = torch.unique(z0[picks]).cpu().numpy().astype(np.uint64)
+    bounds = np.concatenate([[0], zb, [1 << 48]]).astype(np.uint64)
+    nr = len(bounds) - 1
+    starts = torch.searchsorted(z0, torch.from_numpy(bounds.astype(np.int64)).to(cuda)).cpu().numpy()
+
+    # one pass over the raw products in raw-row order: rows per range
+    az0, bz0 = a[1][:, 0], b[1][:, 0]
+    per = [[] for _ in range(nr)]
+    step = 500
+    for js in range(0, mb, step):
+        je = min(mb, js + step)
+        zz = (bz0[js:je, None] ^ az0[None, :]).reshape(-1)
+        rid = np.searchsorted(zb, zz, side="right").astype(np.int16)
+        order = np.argsort(rid, kind="stable")
+        cuts = np.concatenate([[0], np.cumsum(np.bincount(rid, minlength=nr))])
+        for r in range(nr):
+            if cuts[r + 1] > cuts[r]:
+                per[r].append(js * ma + order[cuts[r]:cuts[r + 1]].astype(np.int64))
+    assert sum(sum(len(p) for p in ps) for ps in per) == ma * mb
+
+    def check(r):
+        rows = np.concatenate(per[r]) if per[r] else np.zeros(0, np.int64)
+        ex, ez, _, ec = R.combine(*R.outer_raw_rows(*a, *b, rows))
+        s, e = int(starts[r]), int(starts[r + 1])
+        gx, gz, gk, gc = pl.sums._new_sum(500, out.x[:, s:e], out.z[:, s:e], out.flags[s:e],
+                                          out.coeffs[s:e]).columns()
+        ok = e - s == ex.shape[0] and np.array_equal(gx, ex) and np.array_equal(gz, ez)
+        err = float(np.abs(gc - ec).max(initial=0)) if ok else np.inf
+        return r, ok, err, float(np.abs(ec).sum()), e - s, ex.shape[0]
+
+    with ThreadPoolExecutor(4) as pool:
+        results = list(pool.map(check, range(nr)))
+    bad = [r for r in results if not r[1] or r[2] > TOL * max(r[3], 1e-300)]
+    assert not bad, bad[:5]
+    assert int(starts[-1]) == m
+
+
+def test_c5_simplify_full(cuda):
+    x, z, f, c = rng.c5_columns(1_000_000)
+    got = pl.sort_and_combine(soa(500, (x, z, f, c), cuda))
+    ex, ez, ek, ec = R.combine(x, z, f, c)
+    gx, gz, gk, gc = got.columns()
+    assert np.array_equal(gx, ex) and np.array_equal(gz, ez) and not gk.any()
+    assert np.abs(gc - ec).max() <= TOL * np.abs(ec).sum()
+
+
+def _oracle_rows(x, z, r0, rows):
+    bits = np.concatenate([R.bitmatrix(x, z, r0, r0 + rows, c0, min(x.shape[0], c0 + 40_000))
+                           for c0 in range(0, x.shape[0], 40_000)], axis=1)
+    return R.pack_bitrows(bits)
+
+
+def test_c5_bitmatrix_windows(cuda):
+    x, z, f, c = rng.c5_columns(1_000_000)
+    S = soa(500, (x, z, f, c), cuda)
+    M, chunk = len(S), 65536
+    for c0 in (0, 7 * chunk, (M // chunk) * chunk):  # first, a middle and the partial last chunk
+        rows = min(chunk, M - c0)
+        words = pl.commutation_bitmatrix(S, row0=c0, rows=rows)
+        for off in sorted({0, 1, 1000, rows // 2 + 3, rows - 64}):
+            got = words[off:off + 64].cpu().numpy().view(np.uint32)
+            assert np.array_equal(got, _oracle_rows(x, z, c0 + off, 64)), (c0, off)
+        del words
+
+
+def test_c5_grouping_full_and_prefix(cuda):
+    from oracle import cgreedy
+
+    x, z, f, c = rng.c5_columns(1_000_000)
+    pre = 20_000
+    gof_ref, ng_ref, pc_ref = cgreedy.greedy(x[:pre], z[:pre])
+    S = soa(500, (x[:pre], z[:pre], f[:pre], c[:pre]), cuda)
+    st = pl.GroupingStats()
+    part = pl.group_greedy(S, stats=st)
+    gof = np.zeros(pre, np.int32)
+    for gi, g in enumerate(part.groups):
+        gof[g] = gi
+    assert np.array_equal(gof, gof_ref) and st.pair_checks == pc_ref
+    full = pl.group_assignment(soa(500, (x, z, f, c), cuda))
+    gfull = full[0].cpu().numpy()
+    assert np.array_equal(gfull[:pre], gof_ref)
+    assert int(full[1].item()) == int(gfull.max()) + 1
+    assert int(full[2].item()) == R.pair_checks_from_assignment(gfull)
