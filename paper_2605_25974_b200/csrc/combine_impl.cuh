@@ -45,7 +45,12 @@
 namespace plb {
 
 constexpr int kGenThreads = 256;
-constexpr int kGenTB = 16;        // b-terms per tile (outer) / terms per thread (sort)
+constexpr int kGenTB = 16;        // items per thread: b-terms of its group (outer) / terms (sort)
+// outer-product tiles: kTileA sorted A-terms x kTileB sorted B-terms per CTA;
+// thread t takes A-term t % kTileA and the kGenTB B-terms of group t / kTileA
+constexpr int kTileA = 64;
+constexpr int kTileB = kGenThreads / kTileA * kGenTB;  // 64
+constexpr int kSortOpsChunk = 16384;  // operand terms per k_sort_ops CTA (14-bit local index)
 constexpr int kLeafThreads = 1024;  // k_sample (one-CTA sample sort)
 constexpr int kSplitThreads = 1024;
 constexpr int kSortSmemBytes = 200 * 1024;
@@ -90,6 +95,7 @@ struct Ctl {  // control arrays inside the workspace
   u64* opk;               // [KW][ma (+ mb)] packed operand keys
   uint8_t* opb;           // [ma (+ mb)] operand base phases
   uint16_t* l1tab;        // 2^kTabBits + 1: first splitter per top-bit prefix
+  int32_t* perm;          // outer: [ma + mb] sorted position -> operand index (A, then B)
   u64* k1;               // [KW][n] item keys, buffer 1
   uint32_t* i1;          // [n]
   u64* k2;               // buffer 2
@@ -541,9 +547,10 @@ struct GenSmem {
   u64* split;
   uint32_t* hist;
   uint32_t* gbase;
-  u64* tile;       // outer: [2W][kGenTB] b-term words (z then x)
-  u64* tkey;       // outer: [KW][kGenTB] packed b-term keys
-  uint32_t* tpb;   // outer: [kGenTB] b-term base phases
+  u64* tile;       // outer: [2W][kTileB] b-term words (z then x)
+  u64* tkey;       // outer: [KW][kTileB] packed b-term keys
+  uint32_t* tpb;   // outer: [kTileB] b-term base phases
+  uint32_t* tj;    // outer: [kTileB] b-term operand index (raw row = j * ma + i)
   uint32_t* slot;  // per item: bucket << 16 | rank  (scatter only)
   uint16_t* tab;   // level-1 prefix table (2^kTabBits + 1)
 };
@@ -555,16 +562,17 @@ __device__ __forceinline__ GenSmem gen_smem(u64* sm, int nb1, int KW) {
   g.hist = reinterpret_cast<uint32_t*>(sm + (int64_t)KW * nb1);
   g.gbase = g.hist + nb1;
   g.tile = reinterpret_cast<u64*>(g.gbase + nb1);  // 2*nb1 u32 keeps 8-byte alignment
-  g.tkey = g.tile + 2 * W * kGenTB;
-  g.tpb = reinterpret_cast<uint32_t*>(g.tkey + KW * kGenTB);
-  g.slot = g.tpb + kGenTB;
+  g.tkey = g.tile + 2 * W * kTileB;
+  g.tpb = reinterpret_cast<uint32_t*>(g.tkey + KW * kTileB);
+  g.tj = g.tpb + kTileB;
+  g.slot = g.tj + kTileB;
   g.tab = reinterpret_cast<uint16_t*>(g.slot + kGenTB * kGenThreads);
   return g;
 }
 
 __host__ __device__ constexpr size_t gen_smem_bytes(int W, int KW, int nb1) {
-  return (size_t)8 * KW * nb1 + 8 * (size_t)nb1 + (size_t)16 * W * kGenTB +
-         (size_t)8 * KW * kGenTB + 4 * (size_t)kGenTB + (size_t)4 * kGenTB * kGenThreads +
+  return (size_t)8 * KW * nb1 + 8 * (size_t)nb1 + (size_t)16 * W * kTileB +
+         (size_t)8 * KW * kTileB + 8 * (size_t)kTileB + (size_t)4 * kGenTB * kGenThreads +
          2 * (size_t)((1 << kTabBits) + 1) + 64;
 }
 
@@ -580,7 +588,16 @@ __device__ __forceinline__ void gen_prologue(const GenSmem& g, const Ctl& C, int
   }
 }
 
-// Per-thread item generator.  Outer: thread = a-term i, items (i, j0+jj).
+// Per-thread item generator.
+// Outer: the CTA owns the tile (sorted A positions [blockIdx.x*kTileA, +kTileA)) x
+// (sorted B positions [blockIdx.y*kTileB, +kTileB)).  Operands are visited in
+// packed-key order (C.perm, k_sort_ops), so a tile's products share a long key
+// prefix and land in a few level-1 buckets: the bucket runs written per CTA are
+// long (coalesced) instead of ~8 items in each of 512 buckets.  Thread t takes
+// A-term t % kTileA and the kGenTB B-terms of group t / kTileA; a warp's lanes
+// share the B-term of every step (shared-memory broadcast).  Raw rows use the
+// ORIGINAL operand indices (raw row j*Ma + i, sums.py:137), so the (key, ik)
+// order and every run sum are unchanged.
 // Sort: thread handles terms base + jj*blockDim + tid.
 template <int W, int KW, int MODE>
 struct Gen {
@@ -592,29 +609,33 @@ struct Gen {
   __device__ __forceinline__ void init(const Layout& L, const Dims& D, const SrcA& S,
                                        const Ctl& C, const GenSmem& g) {
     if (MODE == 0) {
-      i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-      valid_i = i < D.ma;
+      const int64_t is = (int64_t)blockIdx.x * kTileA + (threadIdx.x % kTileA);
+      valid_i = is < D.ma;
+      i = valid_i ? C.perm[is] : 0;
       const int64_t nops = D.ma + D.mb_all;
-      const int64_t j0 = D.j0 + (int64_t)blockIdx.y * kGenTB;
-      // b tile into shared memory: active z words then x words, packed keys, base phases
-      for (int t = threadIdx.x; t < 2 * W * kGenTB; t += blockDim.x) {
-        const int s = t / kGenTB, jj = t % kGenTB;
+      const int64_t js0 = (int64_t)blockIdx.y * kTileB;  // local sorted B position
+      // b tile into shared memory: operand index, active z words then x words,
+      // packed keys, base phases
+      for (int jj = threadIdx.x; jj < kTileB; jj += blockDim.x) {
+        const int64_t js = js0 + jj;
+        g.tj[jj] = js < D.mb ? (uint32_t)C.perm[D.ma + js] : 0u;
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < 2 * W * kTileB; t += blockDim.x) {
+        const int s = t / kTileB, jj = t % kTileB;
         const int w = s < W ? s : s - W;
-        const int64_t j = j0 + jj;
+        const int64_t j = g.tj[jj];
         u64 v = 0;
-        if (j < D.j0 + D.mb && (L.active >> w & 1))
+        if (js0 + jj < D.mb && (L.active >> w & 1))
           v = s < W ? S.bz[w * S.ldb + j] : S.bx[w * S.ldb + j];
-        g.tile[s * kGenTB + jj] = v;
+        g.tile[s * kTileB + jj] = v;
       }
-      for (int t = threadIdx.x; t < KW * kGenTB; t += blockDim.x) {
-        const int d = t / kGenTB, jj = t % kGenTB;
-        const int64_t j = j0 + jj;
-        g.tkey[t] = j < D.j0 + D.mb ? C.opk[d * nops + D.ma + j] : 0ull;
+      for (int t = threadIdx.x; t < KW * kTileB; t += blockDim.x) {
+        const int d = t / kTileB, jj = t % kTileB;
+        g.tkey[t] = js0 + jj < D.mb ? C.opk[d * nops + D.ma + g.tj[jj]] : 0ull;
       }
-      for (int jj = threadIdx.x; jj < kGenTB; jj += blockDim.x) {
-        const int64_t j = j0 + jj;
-        g.tpb[jj] = j < D.j0 + D.mb ? C.opb[D.ma + j] : 0u;
-      }
+      for (int jj = threadIdx.x; jj < kTileB; jj += blockDim.x)
+        g.tpb[jj] = js0 + jj < D.mb ? C.opb[D.ma + g.tj[jj]] : 0u;
 #pragma unroll
       for (int w = 0; w < W; ++w) {
         const bool on = valid_i && (L.active >> w & 1);
@@ -633,19 +654,19 @@ struct Gen {
     int64_t r;
     int k;
     if (MODE == 0) {
-      const int64_t j = D.j0 + (int64_t)blockIdx.y * kGenTB + jj;  // global B index
-      if (!valid_i || j >= D.j0 + D.mb) return false;
-      k = pa + (int)g.tpb[jj];
+      const int bb = (threadIdx.x / kTileA) * kGenTB + jj;  // slot in the B tile
+      if (!valid_i || (int64_t)blockIdx.y * kTileB + bb >= D.mb) return false;
+      k = pa + (int)g.tpb[bb];
 #pragma unroll
       for (int w = 0; w < W; ++w) {
         if (L.active >> w & 1) {
-          const u64 b_z = g.tile[w * kGenTB + jj], b_x = g.tile[(W + w) * kGenTB + jj];
+          const u64 b_z = g.tile[w * kTileB + bb], b_x = g.tile[(W + w) * kTileB + bb];
           k += 2 * popc64(az[w] & b_x) - popc64((ax[w] ^ b_x) & (az[w] ^ b_z));
         }
       }
 #pragma unroll
-      for (int d = 0; d < KW; ++d) key[d] = ka[d] ^ g.tkey[d * kGenTB + jj];
-      r = j * D.ma + i;
+      for (int d = 0; d < KW; ++d) key[d] = ka[d] ^ g.tkey[d * kTileB + bb];
+      r = (int64_t)g.tj[bb] * D.ma + i;
     } else {
       r = (int64_t)blockIdx.x * blockDim.x * kGenTB + (int64_t)jj * blockDim.x + threadIdx.x;
       if (r >= D.n) return false;
@@ -657,6 +678,48 @@ struct Gen {
     return true;
   }
 };
+
+// Operand order for the outer-product tiles: each CTA sorts one chunk of up
+// to kSortOpsChunk terms of A (blocks [0, nca)) or of B's local columns (the
+// rest) by the top 50 bits of packed key word 0, via a shared-memory bitonic
+// sort of (key & ~0x3FFF) | local index, and writes sorted position ->
+// operand index into C.perm.  Only the locality of the tiles depends on it.
+template <int KW>
+__global__ void __launch_bounds__(1024) k_sort_ops(Dims D, Ctl C) {
+  extern __shared__ u64 sm[];
+  const int64_t nops = D.ma + D.mb_all;
+  const int nca = (int)ceil_div(D.ma, kSortOpsChunk);
+  const bool isb = (int)blockIdx.x >= nca;
+  const int64_t c0 = (int64_t)(isb ? blockIdx.x - nca : blockIdx.x) * kSortOpsChunk;
+  const int64_t n_all = isb ? D.mb : D.ma;
+  const int n = (int)min((int64_t)kSortOpsChunk, n_all - c0);
+  if (n <= 0) return;
+  // operand index of local position e: A term c0 + e, or B column j0 + c0 + e
+  const int64_t op0 = isb ? D.ma + D.j0 + c0 : c0;
+  int npow = 1;
+  while (npow < n) npow <<= 1;
+  for (int e = threadIdx.x; e < npow; e += blockDim.x)
+    sm[e] = e < n ? ((C.opk[op0 + e] & ~0x3FFFull) | (u64)e) : ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= npow; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < (npow >> 1); t += blockDim.x) {
+        const int a = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const int b = (j == (k >> 1)) ? (a ^ (k - 1)) : (a + j);
+        const u64 va = sm[a], vb = sm[b];
+        if (vb < va) {
+          sm[a] = vb;
+          sm[b] = va;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  int32_t* out = C.perm + (isb ? D.ma : 0) + c0;
+  const int64_t base = isb ? D.j0 + c0 : c0;  // B: global column index
+  for (int e = threadIdx.x; e < n; e += blockDim.x) out[e] = (int32_t)(base + (sm[e] & 0x3FFF));
+  (void)nops;
+}
 
 __device__ __forceinline__ int pow2_floor(int v) { return v > 0 ? 1 << (31 - __clz(v)) : 0; }
 
@@ -703,9 +766,15 @@ k_count(Layout L, Dims D, SrcA S, Ctl C) {
         }
       }
     }
+    // warp-aggregated histogram: a tile's items share few buckets
 #pragma unroll
-    for (int u = 0; u < kGenIlp; ++u)
-      if (ok[u]) atomicAdd(&g.hist[pos[u]], 1u);
+    for (int u = 0; u < kGenIlp; ++u) {
+      const unsigned act = __ballot_sync(0xffffffffu, ok[u]);
+      if (ok[u]) {
+        const unsigned peers = __match_any_sync(act, pos[u]);
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&g.hist[pos[u]], (uint32_t)__popc(peers));
+      }
+    }
   }
   __syncthreads();
   for (int b = threadIdx.x; b < D.nb1; b += blockDim.x)
@@ -753,10 +822,20 @@ k_scatter(Layout L, Dims D, SrcA S, Ctl C) {
         }
       }
     }
+    // warp-aggregated ranks: lanes with the same bucket get consecutive slots
+    const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int u = 0; u < kGenIlp; ++u) {
       uint32_t code = 0xFFFFFFFFu;
-      if (ok[u]) code = ((uint32_t)pos[u] << 16) | atomicAdd(&g.hist[pos[u]], 1u);
+      const unsigned act = __ballot_sync(0xffffffffu, ok[u]);
+      if (ok[u]) {
+        const unsigned peers = __match_any_sync(act, pos[u]);
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(&g.hist[pos[u]], (uint32_t)__popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        code = ((uint32_t)pos[u] << 16) | (base + __popc(peers & ((1u << lane) - 1u)));
+      }
       g.slot[(j0 + u) * kGenThreads + threadIdx.x] = code;
     }
   }
@@ -1059,7 +1138,8 @@ static inline int64_t align256(int64_t v) { return (v + 255) & ~(int64_t)255; }
 
 struct WsLayout {
   int64_t split, bcount, bbase, bcursor, leaf_off, n_leaves, leaf_ctr, tile_off, n_tiles,
-      sub_count, leaf_desc, split2, kept, kprefix, scan, k1, i1, k2, i2, sums, rmap, opk, opb, l1tab, total;
+      sub_count, leaf_desc, split2, kept, kprefix, scan, k1, i1, k2, i2, sums, rmap, opk, opb, l1tab,
+      perm, total;
 };
 
 // Bound on the number of leaves: a bucket of s items gets at most
@@ -1101,6 +1181,7 @@ static WsLayout ws_layout(const pl_merge_plan& P) {
   w.opk = o; o = align256(o + 8 * KW * (P.ma + P.mb));
   w.opb = o; o = align256(o + (P.ma + P.mb));
   w.l1tab = o; o = align256(o + 2 * ((1 << kTabBits) + 1));
+  w.perm = o; o = align256(o + 4 * (P.ma + P.mb));
   w.total = o;
   (void)ctl_end;
   return w;
@@ -1314,6 +1395,7 @@ static Ctl to_ctl(const pl_merge_plan& P, void* ws) {
   C.opk = (u64*)(b + w.opk);
   C.opb = (uint8_t*)(b + w.opb);
   C.l1tab = (uint16_t*)(b + w.l1tab);
+  C.perm = (int32_t*)(b + w.perm);
   C.k1 = (u64*)(b + w.k1);
   C.i1 = (uint32_t*)(b + w.i1);
   C.k2 = (u64*)(b + w.k2);
@@ -1321,6 +1403,20 @@ static Ctl to_ctl(const pl_merge_plan& P, void* ws) {
   return C;
 }
 
+
+template <int KW>
+static int launch_sort_ops(const Dims& D, const Ctl& C, cudaStream_t st) {
+  const int64_t nmax = std::min<int64_t>(kSortOpsChunk, std::max(D.ma, D.mb));
+  int npow = 1;
+  while (npow < nmax) npow <<= 1;
+  const size_t sm = 8 * (size_t)npow;
+  if (set_smem(k_sort_ops<KW>, sm)) return PL_ERR_CUDA;
+  const unsigned nblk = (unsigned)(ceil_div(D.ma, kSortOpsChunk) + ceil_div(D.mb, kSortOpsChunk));
+  StageTimer t_(st, "k_sort_ops");
+  k_sort_ops<KW><<<nblk, 1024, sm, st>>>(D, C);
+  PLB_CHECK_LAUNCH("k_sort_ops");
+  return PL_OK;
+}
 
 template <int W, int KW, int MODE>
 static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const OutP& O,
@@ -1338,6 +1434,10 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const O
                               0, st>>>(L, S, D.ma, D.mb_all, C);
     PLB_CHECK_LAUNCH("k_pack_ops");
   }
+  if (MODE == 0) {
+    const int rc = launch_sort_ops<KW>(D, C, st);
+    if (rc) return rc;
+  }
   // 1-2. splitters + counts
   if (D.nb1 > 1) {
     const size_t sm1 = (size_t)D.nsamp * (8 * KW + 4) + 16;
@@ -1353,7 +1453,7 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const O
   }
   const size_t gsm = gen_smem_bytes(W, KW, D.nb1);
   dim3 ggrid;
-  if (MODE == 0) ggrid = dim3((unsigned)ceil_div(D.ma, kGenThreads), (unsigned)ceil_div(D.mb, kGenTB));
+  if (MODE == 0) ggrid = dim3((unsigned)ceil_div(D.ma, kTileA), (unsigned)ceil_div(D.mb, kTileB));
   else ggrid = dim3((unsigned)ceil_div(D.n, (int64_t)kGenThreads * kGenTB), 1);
   if (ggrid.y > 65535) {
     set_error("outer product: |B| too large for one call (%lld)", (long long)D.mb);
@@ -1475,6 +1575,10 @@ static int run_partition(const pl_merge_plan& P, const SrcA& S, int64_t j0, int6
                              0, st>>>(L, S, D.ma, D.mb_all, C);
       PLB_CHECK_LAUNCH("k_pack_ops");
     }
+    {
+      const int rc = launch_sort_ops<KW>(D, C, st);
+      if (rc) return rc;
+    }
     if (D.nb1 > 1) {
       const size_t sm1 = (size_t)D.nsamp * (8 * KW + 4) + 16;
       if (set_smem(k_sample<W, KW, 0>, sm1)) return PL_ERR_CUDA;
@@ -1488,7 +1592,7 @@ static int run_partition(const pl_merge_plan& P, const SrcA& S, int64_t j0, int6
       PLB_CHECK_LAUNCH("k_l1_table");
     }
     const size_t gsm = gen_smem_bytes(W, KW, D.nb1);
-    const dim3 ggrid((unsigned)ceil_div(D.ma, kGenThreads), (unsigned)ceil_div(D.mb, kGenTB));
+    const dim3 ggrid((unsigned)ceil_div(D.ma, kTileA), (unsigned)ceil_div(D.mb, kTileB));
     if (D.nb1 > 1) {
       if (set_smem(k_count<W, KW, 0>, gsm)) return PL_ERR_CUDA;
       StageTimer t_(st, "k_count");
