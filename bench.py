@@ -37,8 +37,8 @@ L2_FLUSH_BYTES = 512 << 20
 
 
 # kernels launched under one stage-timer entry of the native library
-# (k_split: prep, count, bases, scatter; k_leaf_scan: the 3-kernel scan)
-KERNELS_PER_STAGE = {"k_split": 4, "k_leaf_scan": 3, "k_regroup": 3}
+# (k_leaf_scan: the 3-kernel scan; k_regroup: prep, buckets, copy)
+KERNELS_PER_STAGE = {"k_leaf_scan": 3, "k_regroup": 3}
 
 
 def measured_peaks():
@@ -366,8 +366,8 @@ def main():
     term_b = 16 * 8 + 1 + 16                  # SoA output term at W=8
     algo = {
         "k_scatter": (local_items * item_b, f"{item_b} B item written"),
-        "k_split": (3 * local_items * item_b,
-                    f"{item_b} B item read twice (classify, move) + written once"),
+        "k_split_count": (local_items * 8 * kw, f"{8 * kw} B item key read"),
+        "k_split_scatter": (2 * local_items * item_b, f"{item_b} B item read + written"),
         "k_leaf_sort": (local_items * item_b + local_out * ent_b,
                         f"{item_b} B item read + {ent_b} B (key, sum) per merged term written"),
         "k_emit": (local_out * (ent_b + term_b),

@@ -1113,13 +1113,22 @@ static int launch_split(const pl_merge_plan& P, const Dims& D, const Ctl& C, cud
   if (set_smem(k_split_count<KW>, tsm)) return PL_ERR_CUDA;
   if (set_smem(k_split_scatter<KW>, tsm)) return PL_ERR_CUDA;
   const unsigned max_tiles = (unsigned)(ceil_div(D.n, (int64_t)kSplitTile) + D.nb1);
-  StageTimer t_(st, "k_split");
-  k_split_prep<KW><<<D.nb1, kSplitThreads, psm, st>>>(D, C, s2cap);
-  PLB_CHECK_LAUNCH("k_split_prep");
-  k_split_count<KW><<<max_tiles, kSplitTileThreads, tsm, st>>>(D, C);
-  PLB_CHECK_LAUNCH("k_split_count");
-  k_split_bases<<<D.nb1, 1024, 0, st>>>(D, C);
-  PLB_CHECK_LAUNCH("k_split_bases");
+  {
+    StageTimer t_(st, "k_split_prep");
+    k_split_prep<KW><<<D.nb1, kSplitThreads, psm, st>>>(D, C, s2cap);
+    PLB_CHECK_LAUNCH("k_split_prep");
+  }
+  {
+    StageTimer t_(st, "k_split_count");
+    k_split_count<KW><<<max_tiles, kSplitTileThreads, tsm, st>>>(D, C);
+    PLB_CHECK_LAUNCH("k_split_count");
+  }
+  {
+    StageTimer t_(st, "k_split_bases");
+    k_split_bases<<<D.nb1, 1024, 0, st>>>(D, C);
+    PLB_CHECK_LAUNCH("k_split_bases");
+  }
+  StageTimer t_(st, "k_split_scatter");
   k_split_scatter<KW><<<max_tiles, kSplitTileThreads, tsm, st>>>(D, C);
   PLB_CHECK_LAUNCH("k_split_scatter");
   return PL_OK;
