@@ -118,7 +118,17 @@ struct SrcA {  // operands (outer: A and B; sort: A only)
   const uint8_t* bk;
   const double2* bc;
   int64_t ldb;
+  u64 ma_inv;  // outer: ceil(2^62 / |A|), raw row -> j by multiply (div_ma)
 };
+
+// ceil(2^62 / ma): floor(r * inv / 2^62) == r / ma for every r < 2^30
+inline u64 ma_inverse(int64_t ma) { return ma > 0 ? ((1ull << 62) - 1) / (u64)ma + 1 : 0; }
+
+__device__ __forceinline__ uint32_t div_ma(uint32_t r, u64 inv) {
+  const u64 lo = (u64)r * inv;
+  const u64 hi = __umul64hi((u64)r, inv);
+  return (uint32_t)((hi << 2) | (lo >> 62));
+}
 
 struct OutP {
   u64 *ox, *oz;
@@ -363,7 +373,7 @@ struct Source {
   static __device__ __forceinline__ double2 coef(const SrcA& S, int64_t ma, uint32_t ik) {
     const int64_t r = ik >> 2;
     if (MODE == 0) {
-      const int64_t j = (uint32_t)r / (uint32_t)ma, i = r - j * ma;
+      const int64_t j = div_ma((uint32_t)r, S.ma_inv), i = r - j * ma;
       return rot_ik(cmul_np(S.ac[i], S.bc[j]), (int)(ik & 3));
     } else {
       return rot_ik(S.ac[r], (int)(ik & 3));
@@ -1428,8 +1438,10 @@ static int launch_sort_ops(const Dims& D, const Ctl& C, cudaStream_t st) {
 }
 
 template <int W, int KW, int MODE>
-static int run_pipeline(const pl_merge_plan& P, const SrcA& S, void* ws, const OutP& O,
+static int run_pipeline(const pl_merge_plan& P, const SrcA& S0, void* ws, const OutP& O,
                         cudaStream_t st) {
+  SrcA S = S0;
+  S.ma_inv = ma_inverse(P.ma);
   const Layout L = to_layout(P);
   const Dims D = to_dims(P);
   const Ctl C = to_ctl(P, ws);
@@ -1629,8 +1641,10 @@ static int run_partition(const pl_merge_plan& P, const SrcA& S, int64_t j0, int6
 
 template <int W, int KW>
 static int run_merge_received(const pl_merge_plan& P, const u64* recv, int64_t n_recv,
-                              const uint32_t* cnt, int G, int nbl, const SrcA& S, void* ws,
+                              const uint32_t* cnt, int G, int nbl, const SrcA& S0, void* ws,
                               const OutP& O, cudaStream_t st) {
+  SrcA S = S0;
+  S.ma_inv = ma_inverse(P.ma);
   const pl_merge_plan Q = local_plan(P, n_recv, nbl);
   const Layout L = to_layout(Q);
   Dims D = to_dims(Q);
