@@ -183,7 +183,9 @@ int pl_sort_combine(const pl_merge_plan* plan,
  * c in [col0, col0+cols).  Rows and columns index the same M-term sum.
  * col0 must be a multiple of 32; trailing bits of the last word are 0.
  * method: 0 = auto, 1 = row-list XOR over transposed column slices
- * (sparse-friendly), 2 = direct LOP3/POPC per pair.
+ * (sparse-friendly), 2 = direct LOP3/POPC per pair, 3 = tensor cores
+ * (tcgen05.mma.kind::i8 on 0/1 byte expansions, K = 128 W; W <= 8).  Auto
+ * takes 1 for sparse rows and 3 above ~24 W letters per row (W <= 8).
  */
 int pl_commutation_bitmatrix(int W, int64_t M,
                              const uint64_t* x, const uint64_t* z, int64_t ld,

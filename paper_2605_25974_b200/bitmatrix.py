@@ -14,7 +14,7 @@ from . import _native
 from ._device import plane_ld, ptr, stream_ptr
 from .sums import PauliSumSoA, _compute_device
 
-METHODS = {"auto": 0, "lists": 1, "direct": 2}
+METHODS = {"auto": 0, "lists": 1, "direct": 2, "tensor": 3}
 
 
 def words_per_row(cols: int) -> int:

@@ -11,16 +11,23 @@
 // row, 16 lanes x 64 columns).  The rows' letter lists (CSR, built once per
 // call) are staged per warp 16 rows at a time and prefetched one block
 // ahead.  Cost per 1024 checks is proportional to the row weight (config 5:
-// weight 2-12), far below the 4W LOP3 + POPC per check of method 2; the
-// tensor-core formulation (int8 expansions, K = 128W) would cost 2048 ops per
-// check and is not used.
+// weight 2-12), far below the 4W LOP3 + POPC per check of method 2 and the
+// 256 W int8 tensor ops per check of method 3.
 //
 // Method 2 (direct).  One thread per row, the row's 2W words in registers,
 // columns broadcast from shared memory: 4W LOP3 + POPC per check.  Used for
 // dense rows and W = 16 (whose slices exceed shared memory).
+//
+// Method 3 (tensor, bitmatrix_tc.cuh): the int8 GEMM formulation on
+// tcgen05.mma.kind::i8 for dense rows, W <= 8: 1.4-1.5x method 2 on uniform
+// random strings (W=8: 6.4e11 vs 4.5e11 checks/s; the LOP3 roofline of method
+// 2 is 5.4e11), chosen by "auto" above ~24 W letters per row.  The legacy
+// binary MMA (mma.sync m16n8k256 b1 AND.POPC) compiles to an int8 emulation
+// on sm_100a (MOVM.U4TO8 + IMMA) and is not used.
 #include "common.cuh"
 #include "scan.cuh"
 #include "bitmatrix_kernels.cuh"
+#include "bitmatrix_tc.cuh"
 
 namespace plb {
 
@@ -32,9 +39,25 @@ static int launch_bitmatrix(int64_t M, const u64* x, const u64* z, int64_t ld, i
                             int64_t rows, int64_t col0, int64_t cols, uint32_t* bits,
                             int64_t ld_bits, int method, void* ws, size_t ws_bytes,
                             cudaStream_t st) {
-  if (W == 16 && method == 1) {
-    set_error("bitmatrix method 1 supports W <= 8");
+  if (W == 16 && (method == 1 || method == 3)) {
+    set_error("bitmatrix methods 1 and 3 support W <= 8");
     return PL_ERR_ARG;
+  }
+  if constexpr (W <= 8) if (method == 3) {
+    const size_t smem = TcSmem<W>::BYTES;
+    auto kern = k_bitmatrix_tc<W>;
+    PLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t colblocks = ceil_div(cols, kTcCols);
+    const int64_t rowblocks = ceil_div(rows, kTcRows);
+    for (int64_t rb = 0; rb < rowblocks; rb += 65535) {
+      const int64_t nrb = rowblocks - rb < 65535 ? rowblocks - rb : 65535;
+      StageTimer t_(st, "k_bitmatrix_tc");
+      kern<<<dim3((unsigned)colblocks, (unsigned)nrb), kTcThreads, smem, st>>>(
+          x, z, ld, M, row0 + rb * kTcRows, rows - rb * kTcRows, col0, cols,
+          bits + rb * kTcRows * ld_bits, ld_bits);
+      PLB_CHECK_LAUNCH("k_bitmatrix_tc");
+    }
+    return PL_OK;
   }
   if (method != 2 && W <= 8) {
     // CSR row lists: off (rows+1) u32 | scan scratch | list u16
@@ -66,15 +89,18 @@ static int launch_bitmatrix(int64_t M, const u64* x, const u64* z, int64_t ld, i
     PLB_CUDA(cudaMemcpyAsync(&total, off + rows, 4, cudaMemcpyDeviceToHost, st));
     PLB_CUDA(cudaStreamSynchronize(st));
     const double avg = rows ? (double)total / (double)rows : 0.0;
-    // method 1 costs ~1 LDS per set bit per 32 checks; method 2 ~4W LOP3 per check
-    const bool dense = avg > 48.0 * W;
+    // method 1 costs ~1 shared load per letter per 64 checks; method 3 (tensor)
+    // 256 W int8 ops per check whatever the density.  Measured crossover on
+    // B200 (profiles/r2/bitmatrix_pipes.json): ~24 W letters per row
+    const bool dense = avg > 24.0 * W;
     if ((int64_t)total > cap || (method == 0 && dense)) {
       if (method == 1) {
         set_error("bitmatrix: list workspace too small (%u entries > %lld)", total,
                   (long long)cap);
         return PL_ERR_WORKSPACE;
       }
-      method = 2;
+      return launch_bitmatrix<W>(M, x, z, ld, row0, rows, col0, cols, bits, ld_bits, 3, ws,
+                                 ws_bytes, st);
     } else {
       k_row_fill<W, 2><<<nb, 256, 0, st>>>(x, z, ld, row0, rows, off, list);
       PLB_CHECK_LAUNCH("k_row_fill");
@@ -132,7 +158,7 @@ extern "C" int pl_commutation_bitmatrix(int W, int64_t M, const uint64_t* x, con
                                         void* workspace, size_t workspace_bytes, void* stream) {
   if (M < 0 || ld < M || row0 < 0 || rows < 0 || row0 + rows > M || col0 < 0 || cols < 0 ||
       col0 + cols > M || (col0 % 32) != 0 || ld_bits < ceil_div(cols, 32) || method < 0 ||
-      method > 2) {
+      method > 3) {
     set_error("pl_commutation_bitmatrix: bad arguments");
     return PL_ERR_ARG;
   }

@@ -1,6 +1,7 @@
 """GPU parity: K5 commutation bitmatrix (both methods) vs the reference/oracle."""
 
 import numpy as np
+import torch
 import pytest
 
 from conftest import golden
@@ -12,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("name", ["bitmatrix_c5", "bitmatrix_dense100"])
-@pytest.mark.parametrize("method", ["lists", "direct", "auto"])
+@pytest.mark.parametrize("method", ["lists", "direct", "tensor", "auto"])
 def test_bitmatrix_golden(cuda, name, method):
     g = golden(name)
     m = g["x"].shape[0]
@@ -25,11 +26,11 @@ def test_bitmatrix_golden(cuda, name, method):
     assert np.array_equal(words.cpu().numpy().view(np.uint32), R.pack_bitrows(g["bits"]))
 
 
-@pytest.mark.parametrize("method", ["lists", "direct"])
+@pytest.mark.parametrize("method", ["lists", "direct", "tensor", "auto"])
 @pytest.mark.parametrize("W,n", [(1, 50), (2, 100), (4, 256), (8, 500), (16, 1000)])
 def test_bitmatrix_blocks_all_tiers(cuda, method, W, n):
-    if W == 16 and method == "lists":
-        pytest.skip("lists method covers W <= 8")
+    if W == 16 and method in ("lists", "tensor"):
+        pytest.skip("lists and tensor methods cover W <= 8")
     m = 2500
     x, z, _, _ = rng.random_columns(n, m, 31 + W)
     # sparsify half the rows so both sparse and dense rows occur
@@ -62,3 +63,18 @@ def test_bitmatrix_config5_row_sample(cuda):
     # symmetry of the full matrix
     full = pl.unpack_bits(words[:2048], 20000)[:, :2048].cpu().numpy()
     assert np.array_equal(full, full.T)
+
+
+@pytest.mark.parametrize("n", [64, 100, 200, 500])
+def test_bitmatrix_tensor_dense_auto(cuda, n):
+    """Dense rows (uniform random strings): 'auto' takes the tcgen05 int8 path;
+    every method agrees bit for bit, sampled rows match the oracle."""
+    m = 3000
+    x, z, _, _ = rng.random_columns(n, m, 77)
+    s = pl.PauliSumSoA.from_columns(n, x, z, np.zeros(m, np.uint8), np.ones(m, np.complex128),
+                                    device=cuda)
+    words = {meth: pl.commutation_bitmatrix(s, method=meth) for meth in ("auto", "tensor", "direct")}
+    assert torch.equal(words["auto"], words["tensor"]) and torch.equal(words["tensor"], words["direct"])
+    for r in (0, 127, 128, 1500, m - 1):
+        exp = R.pack_bitrows(R.bitmatrix(x, z, r, r + 1, 0, m))
+        assert np.array_equal(words["tensor"][r:r + 1].cpu().numpy().view(np.uint32), exp)
