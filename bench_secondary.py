@@ -138,6 +138,50 @@ def c3(dev, flush):
                             "ms_per_step": t, "groups": int(ng.item()), "pair_checks": checks}}
 
 
+def c5_grouping(dev, flush):
+    """Config 5 greedy grouping at its full size (10^6 terms, n=500, W=8)."""
+    x, z, f, c = rng.c5_columns(1_000_000, seed=4)
+    S = pl.PauliSumSoA.from_columns(500, x, z, f, c, device=dev)
+    gof, ng, pc = pl.group_assignment(S)
+    ms = _timed(lambda: pl.group_assignment(S), dev, flush, 2, warm=1)
+    t = statistics.mean(ms)
+    checks = int(pc.item())
+    return {"c5_grouping": {"workload": "C5 greedy grouping, 10^6 terms n=500, seed 4",
+                            "value": checks / (t / 1e3), "unit": "reference pair_checks/s",
+                            "ms_per_step": t, "groups": int(ng.item()), "pair_checks": checks}}
+
+
+TC_I8_PEAK = 4.5345e15  # tools/microbench/tc_i8.cu on this pool's B200 (profiles/r2/bitmatrix_pipes.json)
+
+
+def dense_bitmatrix(dev, flush):
+    """K5 on dense rows (uniform random strings, n=500, 65,536 x 65,536 checks):
+    'auto' takes the tcgen05 int8 path; the INT 'direct' path beside it."""
+    M = 65536
+    x, z, f, c = rng.random_columns(500, M, 11)
+    S = pl.PauliSumSoA.from_columns(500, x, z, f, c, device=dev)
+    out = torch.empty((M, M // 32), dtype=torch.int32, device=dev)
+    res = {}
+    for meth in ("auto", "direct"):
+        ms = _timed(lambda: pl.commutation_bitmatrix(S, method=meth, out=out), dev, flush, 3)
+        t = statistics.mean(ms)
+        checks = float(M) * M
+        line = {"workload": f"K5 dense bitmatrix, uniform random n=500, {M} x {M}, method {meth}",
+                "value": checks / (t / 1e3), "unit": "checks/s", "ms_per_step": t}
+        if meth == "auto":
+            ops = checks * 2 * 128 * 8 / (t / 1e3)
+            line["roofline"] = {"bound": "tensor", "achieved": ops / 1e12, "peak": TC_I8_PEAK / 1e12,
+                                "unit": "TOP/s (int8)", "frac": ops / TC_I8_PEAK,
+                                "bytes_per_unit": "2K = 2048 int8 ops per check (K = 128 W)"}
+        else:
+            lop = checks * 34 / (t / 1e3)
+            line["roofline"] = {"bound": "int", "achieved": lop / 1e12, "peak": 18.375,
+                                "unit": "T LOP3/s", "frac": lop / 18.375e12,
+                                "bytes_per_unit": "~34 LOP3 + 1 POPC per check (W=8)"}
+        res["k5_dense_" + meth] = line
+    return res
+
+
 def f3(dev, flush):
     """§8(f) row f3: two-phase parallel grouping of config 3 (8 chunks); the
     partition differs from the sequential greedy one by design, so the group
@@ -249,7 +293,7 @@ def c5_bitmatrix_sharded(dev, flush, group) -> dict:
 
 def run_secondary(dev, flush) -> dict:
     out = {}
-    for fn in (c2, c1, c5, c3, f12, f3):
+    for fn in (c2, c1, c5, c3, c5_grouping, dense_bitmatrix, f12, f3):
         try:
             r = fn(dev, flush)
         except Exception as e:  # keep the headline line even if a side metric fails
