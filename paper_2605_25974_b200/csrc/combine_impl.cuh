@@ -1248,7 +1248,7 @@ static void finish_plan(pl_merge_plan* P, const u64* masks /* z[W] then x[W] */)
   const int KW = P->key_words;
   const int cap = leaf_cap_for(KW);
   P->leaf_cap = cap;
-  P->leaf_target = cap / 3;  // headroom: sampled splitters vary bucket sizes
+  P->leaf_target = KW <= 2 ? cap / 2 : cap / 3;  // headroom for the sampled splitters
   // one-CTA sample capacity: the sampler sorts in up to kSortSmemBytes
   const int scap = std::min(8192, kSortSmemBytes / (8 * KW + 4));
   const int64_t n = P->n_items;
