@@ -524,9 +524,75 @@ __global__ void k_l1_table(Dims D, Ctl C) {
 // term once (and its base phase k + popc(x&z), sums.py:156-157); the item
 // generators then need KW XORs for the key and, per active word, the cross
 // phase 2popc(az&bx) - popc((ax^bx)&(az^bz)) (sums.py:134-136).
+// Sparse key of one term (Layout::sparse): its set bits in packed order (the
+// segments in order, each from its high bit down) appended as sbits-wide
+// values key_bits - p into a bit stream, MSB first, 0-terminated.  One loop
+// over the term's set bits with a segment cursor (the segment words staged in
+// shared memory, so no divergent per-segment loops), a 64-bit accumulator
+// flushed into the key words by a static select.
+template <int W, int KW>
+__device__ __forceinline__ void pack_sparse(const Layout& L, const u64* seg, u64 (&key)[KW]) {
+#pragma unroll
+  for (int d = 0; d < KW; ++d) key[d] = 0;
+  int s = 0;
+  u64 w = seg[0];
+  u64 acc = 0;
+  int fill = 0, wi = 0;  // bits in acc, key word being filled
+  auto flush = [&](u64 v) {
+#pragma unroll
+    for (int d = 0; d < KW; ++d)
+      if (d == wi) key[d] = v;
+    ++wi;
+  };
+  for (;;) {
+    while (w == 0 && s < 2 * W - 1) w = seg[++s];
+    if (w == 0) break;
+    const int hb = 63 - __clzll((long long)w);
+    w ^= 1ull << hb;
+    const int p = L.pos[s] + (L.len[s] - 1 - hb);
+    const u64 v = (u64)(L.key_bits - p);
+    const int nb = L.sbits;
+    if (fill + nb < 64) {
+      acc |= v << (64 - fill - nb);
+      fill += nb;
+    } else {
+      const int r = fill + nb - 64;  // bits spilling into the next word
+      acc |= v >> r;
+      flush(acc);
+      acc = r ? v << (64 - r) : 0ull;
+      fill = r;
+    }
+  }
+  if (fill && wi < KW) flush(acc);  // the zero terminator is the zero tail
+}
+
 template <int W, int KW, int MODE>
-__global__ void k_pack_ops(Layout L, SrcA S, int64_t ma, int64_t mb, Ctl C) {
+__global__ void __launch_bounds__(256) k_pack_ops(Layout L, SrcA S, int64_t ma, int64_t mb, Ctl C) {
   const int64_t n = ma + (MODE == 0 ? mb : 0);
+  if constexpr (MODE == 1 && W <= 8) if (L.sparse) {
+    __shared__ u64 segs[256][2 * W + 1];
+    u64* seg = segs[threadIdx.x];
+    for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x; t0 < n; t0 += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t t = t0 + threadIdx.x;
+      if (t < n) {
+        int base = S.ak ? S.ak[t] : 0;
+#pragma unroll
+        for (int q = 0; q < 2 * W; ++q) {
+          const int w = q < W ? q : q - W;
+          const int len = L.len[q];
+          u64 v = 0;
+          if (len) v = (((q < W ? S.az : S.ax)[w * S.lda + t]) >> L.lo[q]) & low_mask(len);
+          seg[q] = v;
+        }
+        u64 key[KW];
+        pack_sparse<W, KW>(L, seg, key);
+#pragma unroll
+        for (int d = 0; d < KW; ++d) C.opk[d * n + t] = key[d];
+        C.opb[t] = (uint8_t)(base & 3);
+      }
+    }
+    return;
+  }
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
     const bool isb = t >= ma;
@@ -1271,41 +1337,63 @@ static void finish_plan(pl_merge_plan* P, const u64* masks /* z[W] then x[W] */)
   P->workspace_bytes = ws_layout(*P).total;
 }
 
+// OR of every operand word per plane (z[W] then x[W]) and the most set bits
+// (x and z) of any term.  Warp shuffles, then one shared-memory reduction per
+// CTA, then one global atomic per word per CTA.
 template <int W>
-__global__ void k_or_masks(const u64* __restrict__ x, const u64* __restrict__ z, int64_t ld,
-                           int64_t m, u64* out) {
+__global__ void __launch_bounds__(256) k_or_masks(const u64* __restrict__ x,
+                                                  const u64* __restrict__ z, int64_t ld,
+                                                  int64_t m, u64* out) {
+  __shared__ u64 red[8][2 * W + 1];
   u64 mz[W], mx[W];
   unsigned long long maxbits = 0;  // most set bits (x and z) of any term
 #pragma unroll
   for (int w = 0; w < W; ++w) mz[w] = mx[w] = 0;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m;
        t += (int64_t)gridDim.x * blockDim.x) {
+    u64 zv[W], xv[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {  // all 2W loads in flight together
+      zv[w] = __ldg(z + w * ld + t);
+      xv[w] = __ldg(x + w * ld + t);
+    }
     int bitsum = 0;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      const u64 zv = z[w * ld + t], xv = x[w * ld + t];
-      mz[w] |= zv;
-      mx[w] |= xv;
-      bitsum += popc64(zv) + popc64(xv);
+      mz[w] |= zv[w];
+      mx[w] |= xv[w];
+      bitsum += popc64(zv[w]) + popc64(xv[w]);
     }
     maxbits = maxbits > (unsigned long long)bitsum ? maxbits : (unsigned long long)bitsum;
   }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long v = __shfl_xor_sync(0xffffffffu, maxbits, o);
     maxbits = v > maxbits ? v : maxbits;
-  }
-  if ((threadIdx.x & 31) == 0 && maxbits) atomicMax(&out[2 * W], maxbits);
 #pragma unroll
-  for (int w = 0; w < W; ++w) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int w = 0; w < W; ++w) {
       mz[w] |= __shfl_xor_sync(0xffffffffu, mz[w], o);
       mx[w] |= __shfl_xor_sync(0xffffffffu, mx[w], o);
     }
-    if ((threadIdx.x & 31) == 0) {
-      if (mz[w]) atomicOr(&out[w], mz[w]);
-      if (mx[w]) atomicOr(&out[W + w], mx[w]);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      red[warp][w] = mz[w];
+      red[warp][W + w] = mx[w];
+    }
+    red[warp][2 * W] = maxbits;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e <= 2 * W; e += blockDim.x) {
+    u64 v = 0;
+    for (int q = 0; q < (int)(blockDim.x / 32); ++q)
+      v = e < 2 * W ? (v | red[q][e]) : (red[q][e] > v ? red[q][e] : v);
+    if (e < 2 * W) {
+      if (v) atomicOr(&out[e], v);
+    } else if (v) {
+      atomicMax(&out[2 * W], v);
     }
   }
 }
@@ -1315,7 +1403,7 @@ static int launch_masks(const u64* x, const u64* z, int64_t ld, int64_t m, u64* 
                         cudaStream_t st) {
   if (m == 0) return PL_OK;
   int64_t blocks = ceil_div(m, 256);
-  if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
+  if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
   StageTimer t_(st, "k_or_masks");
   k_or_masks<W><<<(unsigned)blocks, 256, 0, st>>>(x, z, ld, m, out);
   PLB_CHECK_LAUNCH("k_or_masks");
