@@ -468,36 +468,116 @@ struct RunSum {
 };
 
 // ------------------------------------------------------------- 1. sampler
+// One CTA: ns deterministic sample keys of the product (raw rows spread
+// evenly), sorted, every (ns/nb1)-th taken as a level-1 splitter.  The sort
+// runs on 64-bit composites (key word 0 with its low 13 bits replaced by the
+// sample index: one compare per exchange instead of KW words + index), then
+// every run of equal composite prefixes is finished on the full keys by
+// insertion sort (rare), so the splitters are exactly the sorted samples.
 template <int W, int KW, int MODE>
 __global__ void __launch_bounds__(kLeafThreads)
 k_sample(Layout L, Dims D, SrcA S, Ctl C) {
   extern __shared__ u64 sm[];
   const int ns = D.nsamp;
-  u64* K = sm;
-  uint32_t* I = reinterpret_cast<uint32_t*>(K + (int64_t)KW * ns);
-  for (int s = threadIdx.x; s < ns; s += blockDim.x) {
-    const int64_t r = ((2 * (int64_t)s + 1) * D.n_space) / (2 * (int64_t)ns);
-    u64 key[KW];
-    // packed keys of the operands are already in C.opk (k_pack_ops)
-    if (MODE == 1) {
+  u64* K = sm;                        // [KW][ns] sample keys
+  u64* CK = K + (int64_t)KW * ns;     // [npow] composites
+  int npow = 1;
+  while (npow < ns) npow <<= 1;
+  for (int s = threadIdx.x; s < npow; s += blockDim.x) {
+    if (s < ns) {
+      const int64_t r = ((2 * (int64_t)s + 1) * D.n_space) / (2 * (int64_t)ns);
+      u64 key[KW];
+      // packed keys of the operands are already in C.opk (k_pack_ops)
+      if (MODE == 1) {
 #pragma unroll
-      for (int d = 0; d < KW; ++d) key[d] = C.opk[d * D.ma + r];
+        for (int d = 0; d < KW; ++d) key[d] = C.opk[d * D.ma + r];
+      } else {
+        const int64_t nops = D.ma + D.mb_all;
+        const int64_t j = r / D.ma, i = r - j * D.ma;
+#pragma unroll
+        for (int d = 0; d < KW; ++d) key[d] = C.opk[d * nops + i] ^ C.opk[d * nops + D.ma + j];
+      }
+      store_key<KW>(K, ns, s, key);
+      CK[s] = (key[0] & ~0x1FFFull) | (u64)s;
     } else {
-      const int64_t nops = D.ma + D.mb_all;
-      const int64_t j = r / D.ma, i = r - j * D.ma;
-#pragma unroll
-      for (int d = 0; d < KW; ++d) key[d] = C.opk[d * nops + i] ^ C.opk[d * nops + D.ma + j];
+      CK[s] = ~0ull;
     }
-    store_key<KW>(K, ns, s, key);
-    I[s] = (uint32_t)s;
   }
   __syncthreads();
-  bitonic_sort<KW>(K, I, ns, ns);
+  for (int k = 2; k <= npow; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < (npow >> 1); t += blockDim.x) {
+        const int a = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const int b = (j == (k >> 1)) ? (a ^ (k - 1)) : (a + j);
+        const u64 va = CK[a], vb = CK[b];
+        if (vb < va) {
+          CK[a] = vb;
+          CK[b] = va;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // runs of equal composite prefixes: insertion sort on the full keys; a run
+  // longer than 64 (word 0 nearly constant) switches to a full-key sort
+  __shared__ int s_long;
+  if (threadIdx.x == 0) s_long = 0;
+  __syncthreads();
+  for (int q = threadIdx.x; q < ns; q += blockDim.x) {
+    const u64 pre = CK[q] >> 13;
+    if ((q > 0 && (CK[q - 1] >> 13) == pre) || q + 1 >= ns || (CK[q + 1] >> 13) != pre) continue;
+    int e = q + 1;
+    while (e < ns && (CK[e] >> 13) == pre && e - q <= 64) ++e;
+    if (e - q > 64) {
+      s_long = 1;
+      continue;
+    }
+    for (int a = q + 1; a < e; ++a) {
+      const u64 v = CK[a];
+      const int va = (int)(v & 0x1FFF);
+      int b = a;
+      while (b > q) {
+        const int vb = (int)(CK[b - 1] & 0x1FFF);
+        bool lt = false;
+#pragma unroll
+        for (int d = 0; d < KW; ++d) {
+          const u64 x = K[d * ns + va], y = K[d * ns + vb];
+          if (x != y) {
+            lt = x < y;
+            break;
+          }
+        }
+        if (!lt) break;
+        CK[b] = CK[b - 1];
+        --b;
+      }
+      CK[b] = v;
+    }
+  }
+  __syncthreads();
+  if (s_long) {  // full-key bitonic sort of (key, sample index)
+    uint32_t* I = reinterpret_cast<uint32_t*>(CK);
+    for (int t = threadIdx.x; t < ns; t += blockDim.x) I[t] = (uint32_t)t;
+    __syncthreads();
+    bitonic_sort<KW>(K, I, ns, ns);
+    for (int b = 1 + threadIdx.x; b < D.nb1; b += blockDim.x) {
+      const int src = (int)(((int64_t)b * ns) / D.nb1);
+#pragma unroll
+      for (int d = 0; d < KW; ++d) C.split[d * D.nb1 + (b - 1)] = K[d * ns + src];
+    }
+    return;
+  }
   for (int b = 1 + threadIdx.x; b < D.nb1; b += blockDim.x) {
-    const int src = (int)(((int64_t)b * ns) / D.nb1);
+    const int src = (int)(CK[((int64_t)b * ns) / D.nb1] & 0x1FFF);
 #pragma unroll
     for (int d = 0; d < KW; ++d) C.split[d * D.nb1 + (b - 1)] = K[d * ns + src];
   }
+}
+
+static inline size_t sample_smem_bytes(int ns, int KW) {
+  int npow = 1;
+  while (npow < ns) npow <<= 1;
+  return (size_t)ns * 8 * KW + (size_t)npow * 8 + 16;
 }
 
 // level-1 prefix table: tab[h] = number of splitters whose top kTabBits bits
@@ -1316,7 +1396,8 @@ static void finish_plan(pl_merge_plan* P, const u64* masks /* z[W] then x[W] */)
   P->leaf_cap = cap;
   P->leaf_target = KW <= 2 ? cap / 2 : cap / 3;  // headroom for the sampled splitters
   // one-CTA sample capacity: the sampler sorts in up to kSortSmemBytes
-  const int scap = std::min(8192, kSortSmemBytes / (8 * KW + 4));
+  int scap = 8192;  // a power of two (13-bit sample index) whose keys + composites fit
+  while ((int64_t)scap * (8 * KW + 8) > kSortSmemBytes) scap >>= 1;
   const int64_t n = P->n_items;
   int64_t nb1 = 1;
   if (n > cap) {
@@ -1549,7 +1630,7 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S0, void* ws, const 
   }
   // 1-2. splitters + counts
   if (D.nb1 > 1) {
-    const size_t sm1 = (size_t)D.nsamp * (8 * KW + 4) + 16;
+    const size_t sm1 = sample_smem_bytes(D.nsamp, KW);
     if (set_smem(k_sample<W, KW, MODE>, sm1)) return PL_ERR_CUDA;
     StageTimer t_(st, "k_sample");
     k_sample<W, KW, MODE><<<1, kLeafThreads, sm1, st>>>(L, D, S, C);
@@ -1689,7 +1770,7 @@ static int run_partition(const pl_merge_plan& P, const SrcA& S, int64_t j0, int6
       if (rc) return rc;
     }
     if (D.nb1 > 1) {
-      const size_t sm1 = (size_t)D.nsamp * (8 * KW + 4) + 16;
+      const size_t sm1 = sample_smem_bytes(D.nsamp, KW);
       if (set_smem(k_sample<W, KW, 0>, sm1)) return PL_ERR_CUDA;
       StageTimer t_(st, "k_sample");
       k_sample<W, KW, 0><<<1, kLeafThreads, sm1, st>>>(L, D, S, C);

@@ -337,3 +337,23 @@ def test_tiny_sums(cuda, m):
         assert len(out) == 0
     else:
         check_combined(out, R.combine(x, z, f, c))
+
+
+def test_sampler_constant_leading_key_word(cuda):
+    """Every term shares its letters on qubits 0..63 (packed key word 0 is the
+    same for all terms): the level-1 sampler's word-0 composites all tie and it
+    must fall back to its full-key sort; result still equals the oracle."""
+    n, m = 300, 40_000
+    x, z, f, c = rng.random_columns(n, m, 91)
+    x[:, 0] = x[0, 0]
+    z[:, 0] = z[0, 0]
+    f = (np.arange(m) % 4).astype(np.uint8)
+    x = np.concatenate([x, x[:5000]])
+    z = np.concatenate([z, z[:5000]])
+    f = np.concatenate([f, f[:5000]])
+    c = np.concatenate([c, -c[:5000]])
+    got = pl.sort_and_combine(soa(n, (x, z, f, c), cuda))
+    ex, ez, ek, ec = R.combine(x, z, f, c)
+    gx, gz, gk, gc = got.columns()
+    assert np.array_equal(gx, ex) and np.array_equal(gz, ez)
+    assert np.abs(gc - ec).max(initial=0) <= 1e-12 * np.abs(ec).sum()
