@@ -162,7 +162,8 @@ def cpu_sample_desc(m: int, threads: int) -> str:
     return (f"first {m} x {m} terms of the C4 inputs ({m * m} pair products) per step, time "
             f"extrapolated to the full 10^8 products as n log n (x{nlogn_scale(m * m, C4_PRODUCTS):.3f}, "
             f"BASELINE.md §3); multiply threaded over {threads} threads (sums.py:158-173), "
-            f"combine single-threaded (sums.py:94-120)")
+            f"combine single-threaded (sums.py:94-120); calibration: one full 10^8 run on this "
+            f"pool's host took 85.8 s vs 80.9 s extrapolated (profiles/r2/cpu_c4_full.json)")
 
 
 def run_reference(args, rank: int, world: int):
