@@ -467,38 +467,24 @@ struct RunSum {
   }
 };
 
-// ------------------------------------------------------------- 1. sampler
-// One CTA: ns deterministic sample keys of the product (raw rows spread
-// evenly), sorted, every (ns/nb1)-th taken as a level-1 splitter.  The sort
-// runs on 64-bit composites (key word 0 with its low 13 bits replaced by the
-// sample index: one compare per exchange instead of KW words + index), then
-// every run of equal composite prefixes is finished on the full keys by
-// insertion sort (rare), so the splitters are exactly the sorted samples.
-template <int W, int KW, int MODE>
-__global__ void __launch_bounds__(kLeafThreads)
-k_sample(Layout L, Dims D, SrcA S, Ctl C) {
-  extern __shared__ u64 sm[];
-  const int ns = D.nsamp;
-  u64* K = sm;                        // [KW][ns] sample keys
-  u64* CK = K + (int64_t)KW * ns;     // [npow] composites
+// ------------------------------------------------- sample sorting (one CTA)
+// Sorts ns keys K[KW][ns] (shared memory) through 64-bit composites CK[npow]:
+// the 64 key bits after the first cp bits (a prefix every key shares) with the
+// low 13 bits replaced by the sample index -- one compare per exchange
+// instead of KW words + index -- then finishes every run of equal composite
+// prefixes on the full keys by insertion sort.  A run longer than 64 (keys
+// equal over those 64 bits) makes it fall back to a full-key bitonic sort.
+// Returns (all threads) the sorted position -> sample index map via `order`:
+// order(p) = CK[p] & 0x1FFF, or p itself after the fallback (K then sorted).
+template <int KW>
+__device__ bool sort_samples(u64* K, int ns, u64* CK, int cp) {
   int npow = 1;
   while (npow < ns) npow <<= 1;
   for (int s = threadIdx.x; s < npow; s += blockDim.x) {
     if (s < ns) {
-      const int64_t r = ((2 * (int64_t)s + 1) * D.n_space) / (2 * (int64_t)ns);
       u64 key[KW];
-      // packed keys of the operands are already in C.opk (k_pack_ops)
-      if (MODE == 1) {
-#pragma unroll
-        for (int d = 0; d < KW; ++d) key[d] = C.opk[d * D.ma + r];
-      } else {
-        const int64_t nops = D.ma + D.mb_all;
-        const int64_t j = r / D.ma, i = r - j * D.ma;
-#pragma unroll
-        for (int d = 0; d < KW; ++d) key[d] = C.opk[d * nops + i] ^ C.opk[d * nops + D.ma + j];
-      }
-      store_key<KW>(K, ns, s, key);
-      CK[s] = (key[0] & ~0x1FFFull) | (u64)s;
+      load_key<KW>(K, ns, s, key);
+      CK[s] = (get_seg<KW>(key, cp, 64) & ~0x1FFFull) | (u64)s;
     } else {
       CK[s] = ~0ull;
     }
@@ -518,8 +504,6 @@ k_sample(Layout L, Dims D, SrcA S, Ctl C) {
       __syncthreads();
     }
   }
-  // runs of equal composite prefixes: insertion sort on the full keys; a run
-  // longer than 64 (word 0 nearly constant) switches to a full-key sort
   __shared__ int s_long;
   if (threadIdx.x == 0) s_long = 0;
   __syncthreads();
@@ -555,29 +539,61 @@ k_sample(Layout L, Dims D, SrcA S, Ctl C) {
     }
   }
   __syncthreads();
-  if (s_long) {  // full-key bitonic sort of (key, sample index)
-    uint32_t* I = reinterpret_cast<uint32_t*>(CK);
-    for (int t = threadIdx.x; t < ns; t += blockDim.x) I[t] = (uint32_t)t;
-    __syncthreads();
-    bitonic_sort<KW>(K, I, ns, ns);
-    for (int b = 1 + threadIdx.x; b < D.nb1; b += blockDim.x) {
-      const int src = (int)(((int64_t)b * ns) / D.nb1);
-#pragma unroll
-      for (int d = 0; d < KW; ++d) C.split[d * D.nb1 + (b - 1)] = K[d * ns + src];
-    }
-    return;
-  }
-  for (int b = 1 + threadIdx.x; b < D.nb1; b += blockDim.x) {
-    const int src = (int)(CK[((int64_t)b * ns) / D.nb1] & 0x1FFF);
-#pragma unroll
-    for (int d = 0; d < KW; ++d) C.split[d * D.nb1 + (b - 1)] = K[d * ns + src];
-  }
+  if (!s_long) return true;
+  uint32_t* I = reinterpret_cast<uint32_t*>(CK);
+  for (int t = threadIdx.x; t < ns; t += blockDim.x) I[t] = (uint32_t)t;
+  __syncthreads();
+  bitonic_sort<KW>(K, I, ns, ns);
+  return false;
+}
+
+__host__ __device__ inline int pow2_ceil(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
 }
 
 static inline size_t sample_smem_bytes(int ns, int KW) {
-  int npow = 1;
-  while (npow < ns) npow <<= 1;
-  return (size_t)ns * 8 * KW + (size_t)npow * 8 + 16;
+  return (size_t)ns * 8 * KW + (size_t)pow2_ceil(ns) * 8 + 16;
+}
+
+// ------------------------------------------------------------- 1. sampler
+// One CTA: ns deterministic sample keys of the product (raw rows spread
+// evenly), sorted, every (ns/nb1)-th taken as a level-1 splitter.  The sort
+// runs on 64-bit composites (key word 0 with its low 13 bits replaced by the
+// sample index: one compare per exchange instead of KW words + index), then
+// every run of equal composite prefixes is finished on the full keys by
+// insertion sort (rare), so the splitters are exactly the sorted samples.
+template <int W, int KW, int MODE>
+__global__ void __launch_bounds__(kLeafThreads)
+k_sample(Layout L, Dims D, SrcA S, Ctl C) {
+  extern __shared__ u64 sm[];
+  const int ns = D.nsamp;
+  u64* K = sm;                        // [KW][ns] sample keys
+  u64* CK = K + (int64_t)KW * ns;     // [npow] composites
+  for (int s = threadIdx.x; s < ns; s += blockDim.x) {
+    const int64_t r = ((2 * (int64_t)s + 1) * D.n_space) / (2 * (int64_t)ns);
+    u64 key[KW];
+    // packed keys of the operands are already in C.opk (k_pack_ops)
+    if (MODE == 1) {
+#pragma unroll
+      for (int d = 0; d < KW; ++d) key[d] = C.opk[d * D.ma + r];
+    } else {
+      const int64_t nops = D.ma + D.mb_all;
+      const int64_t j = r / D.ma, i = r - j * D.ma;
+#pragma unroll
+      for (int d = 0; d < KW; ++d) key[d] = C.opk[d * nops + i] ^ C.opk[d * nops + D.ma + j];
+    }
+    store_key<KW>(K, ns, s, key);
+  }
+  __syncthreads();
+  const bool composite = sort_samples<KW>(K, ns, CK, 0);
+  for (int b = 1 + threadIdx.x; b < D.nb1; b += blockDim.x) {
+    const int pos = (int)(((int64_t)b * ns) / D.nb1);
+    const int src = composite ? (int)(CK[pos] & 0x1FFF) : pos;
+#pragma unroll
+    for (int d = 0; d < KW; ++d) C.split[d * D.nb1 + (b - 1)] = K[d * ns + src];
+  }
 }
 
 // level-1 prefix table: tab[h] = number of splitters whose top kTabBits bits
@@ -1125,19 +1141,39 @@ k_split_prep(Dims D, Ctl C, int s2cap) {
   if (ns > s2cap) ns = s2cap;
   if ((uint32_t)ns > size) ns = (int)size;
   u64* SK = sm;
-  uint32_t* SI = reinterpret_cast<uint32_t*>(SK + (int64_t)KW * ns);
+  u64* CK = SK + (int64_t)KW * ns;
   const u64* K1 = C.k1 + base;
   for (int s = threadIdx.x; s < ns; s += blockDim.x) {
     const int64_t r = ((2 * (int64_t)s + 1) * size) / (2 * (int64_t)ns);
 #pragma unroll
     for (int d = 0; d < KW; ++d) SK[d * ns + s] = K1[d * D.n + r];
-    SI[s] = (uint32_t)s;
+  }
+  // the bucket's keys lie between its level-1 splitters: sort on the 64 bits
+  // after the prefix those two share
+  int cp = 0;
+  {
+    bool found = false;
+#pragma unroll
+    for (int d = 0; d < KW; ++d) {
+      const u64 lo_k = b > 0 ? C.split[d * D.nb1 + b - 1] : 0ull;
+      const u64 hi_k = b < D.nb1 - 1 ? C.split[d * D.nb1 + b] : ~0ull;
+      const u64 x = lo_k ^ hi_k;
+      if (!found) {
+        if (x) {
+          cp += __clzll((long long)x);
+          found = true;
+        } else {
+          cp += 64;
+        }
+      }
+    }
   }
   __syncthreads();
-  bitonic_sort<KW>(SK, SI, ns, ns);
+  const bool composite = sort_samples<KW>(SK, ns, CK, cp);
   u64* SP = C.split2 + (int64_t)b * KW * D.max_sub;
   for (int q = 1 + threadIdx.x; q < nsub; q += blockDim.x) {
-    const int src = (int)(((int64_t)q * ns) / nsub);
+    const int pos = (int)(((int64_t)q * ns) / nsub);
+    const int src = composite ? (int)(CK[pos] & 0x1FFF) : pos;
 #pragma unroll
     for (int d = 0; d < KW; ++d) SP[d * D.max_sub + (q - 1)] = SK[d * ns + src];
   }
@@ -1263,7 +1299,7 @@ k_split_scatter(Dims D, Ctl C) {
 template <int KW>
 static int launch_split(const pl_merge_plan& P, const Dims& D, const Ctl& C, cudaStream_t st) {
   const int s2cap = (int)P.reserved[1];
-  const size_t psm = (size_t)s2cap * (8 * KW + 4) + 16;
+  const size_t psm = sample_smem_bytes(s2cap, KW);
   if (set_smem(k_split_prep<KW>, psm)) return PL_ERR_CUDA;
   const size_t tsm = (size_t)8 * KW * D.max_sub + 8 * (size_t)D.max_sub + 4 * (size_t)kSplitTile + 64;
   if (set_smem(k_split_count<KW>, tsm)) return PL_ERR_CUDA;
@@ -1412,7 +1448,8 @@ static void finish_plan(pl_merge_plan* P, const u64* masks /* z[W] then x[W] */)
   P->n_samples = nb1 > 1 ? (int)std::min<int64_t>(n, std::min<int64_t>(scap, nb1 * kSample1Oversample)) : 0;
   // level-2 sample capacity bounds the sub-bucket count
   // level-2 sample (one CTA, <= 160 KB): >= 8 samples per sub-bucket
-  const int s2cap = std::max(64, std::min(8192, (160 * 1024) / (8 * KW + 4)));
+  int s2cap = 8192;  // power of two (13-bit sample index); keys + composites in 200 KB
+  while (s2cap > 64 && (int64_t)s2cap * (8 * KW + 8) > 200 * 1024) s2cap >>= 1;
   P->max_sub = std::max(1, std::min(1024, s2cap / 8));
   P->reserved[1] = s2cap;
   P->workspace_bytes = ws_layout(*P).total;
