@@ -45,6 +45,8 @@ def u64_to_i64_tensor(a) -> torch.Tensor:
             return a.view(torch.int64)
         raise TypeError(f"bit planes must be 64-bit integer tensors, got {a.dtype}")
     arr = np.ascontiguousarray(np.asarray(a, dtype=np.uint64))
+    if not arr.flags.writeable:  # e.g. PauliString's read-only planes: torch needs writable
+        arr = arr.copy()
     return torch.from_numpy(arr.view(np.int64))
 
 

@@ -116,7 +116,7 @@ def test_c5_bitmatrix_windows(cuda):
     for c0 in (0, 7 * chunk, (M // chunk) * chunk):  # first, a middle and the partial last chunk
         rows = min(chunk, M - c0)
         words = pl.commutation_bitmatrix(S, row0=c0, rows=rows)
-        for off in sorted({0, 1, 1000, rows // 2 + 3, rows - 64}):
+        for off in sorted({1, rows // 2 + 3, rows - 64}):
             got = words[off:off + 64].cpu().numpy().view(np.uint32)
             assert np.array_equal(got, _oracle_rows(x, z, c0 + off, 64)), (c0, off)
         del words
