@@ -132,6 +132,16 @@ int pl_outer_multiply_combine(const pl_merge_plan* plan,
                               uint64_t* ox, uint64_t* oz, uint8_t* ok, double* oc, int64_t ldo,
                               int64_t* out_count, void* stream);
 
+/* Two-phase form of pl_outer_multiply_combine / pl_sort_combine, for an
+ * exactly sized output: called with ox == NULL they stop after merging and
+ * write only *out_count (the merged-term count; the merged entries stay in
+ * the workspace, which must not be reused in between); pl_merge_emit then
+ * writes those terms into output planes of `capacity` >= *out_count columns
+ * (ldo >= capacity; terms past `capacity` are not written). */
+int pl_merge_emit(const pl_merge_plan* plan, void* workspace, size_t workspace_bytes,
+                  uint64_t* ox, uint64_t* oz, uint8_t* ok, double* oc, int64_t ldo,
+                  int64_t capacity, int64_t* out_count, void* stream);
+
 /* ------------------------------------------------------------------------
  * K7 — multi-GPU A*B (no reference equivalent; PAPER.md:712-714 lists
  * distributed memory as future work).  Every rank builds the same plan from

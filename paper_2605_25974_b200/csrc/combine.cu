@@ -84,7 +84,8 @@ extern "C" int pl_outer_multiply_combine(const pl_merge_plan* plan, const uint64
                                          int64_t ldo, int64_t* out_count, void* stream) {
   int rc = check_ws(plan, workspace, workspace_bytes, 0);
   if (rc) return rc;
-  if (eps != eps || ldo < plan->n_items || !out_count) {
+  const bool sort_only = ox == nullptr;  // phase 1: count only, then pl_merge_emit
+  if (eps != eps || (!sort_only && ldo < plan->n_items) || !out_count) {
     set_error("pl_outer_multiply_combine: bad arguments");
     return PL_ERR_ARG;
   }
@@ -96,6 +97,7 @@ extern "C" int pl_outer_multiply_combine(const pl_merge_plan* plan, const uint64
   SrcA S{(const u64*)ax, (const u64*)az, ak, (const double2*)ac, lda,
          (const u64*)bx, (const u64*)bz, bk, (const double2*)bc, ldb};
   OutP O{(u64*)ox, (u64*)oz, ok, (double2*)oc, ldo, out_count, eps};
+  O.phase = sort_only ? 1 : 0;
   return PLB_DISPATCH_W(plan->W, run_outer, *plan, S, workspace, O, st);
 }
 
@@ -106,7 +108,8 @@ extern "C" int pl_sort_combine(const pl_merge_plan* plan, const uint64_t* x, con
                                int64_t* out_count, void* stream) {
   int rc = check_ws(plan, workspace, workspace_bytes, 1);
   if (rc) return rc;
-  if (eps != eps || ldo < plan->n_items || !out_count) {
+  const bool sort_only = ox == nullptr;  // phase 1: count only, then pl_merge_emit
+  if (eps != eps || (!sort_only && ldo < plan->n_items) || !out_count) {
     set_error("pl_sort_combine: bad arguments");
     return PL_ERR_ARG;
   }
@@ -118,7 +121,31 @@ extern "C" int pl_sort_combine(const pl_merge_plan* plan, const uint64_t* x, con
   SrcA S{(const u64*)x, (const u64*)z, k, (const double2*)c, ld,
          nullptr, nullptr, nullptr, nullptr, 0};
   OutP O{(u64*)ox, (u64*)oz, ok, (double2*)oc, ldo, out_count, eps};
+  O.phase = sort_only ? 1 : 0;
   return PLB_DISPATCH_W(plan->W, run_sort, *plan, S, workspace, O, st);
+}
+
+extern "C" int pl_merge_emit(const pl_merge_plan* plan, void* workspace, size_t workspace_bytes,
+                             uint64_t* ox, uint64_t* oz, uint8_t* ok, double* oc, int64_t ldo,
+                             int64_t capacity, int64_t* out_count, void* stream) {
+  if (!plan || (plan->mode != 0 && plan->mode != 1)) {
+    set_error("pl_merge_emit: plan missing");
+    return PL_ERR_ARG;
+  }
+  int rc = check_ws(plan, workspace, workspace_bytes, plan->mode);
+  if (rc) return rc;
+  if (!ox || !oz || !ok || !oc || !out_count || capacity < 0 || ldo < capacity) {
+    set_error("pl_merge_emit: bad arguments");
+    return PL_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (plan->n_items == 0) return PL_OK;
+  SrcA S{};
+  OutP O{(u64*)ox, (u64*)oz, ok, (double2*)oc, ldo, out_count, 0.0};
+  O.phase = 2;
+  O.capacity = capacity;
+  return plan->mode == 0 ? PLB_DISPATCH_W(plan->W, run_outer, *plan, S, workspace, O, st)
+                         : PLB_DISPATCH_W(plan->W, run_sort, *plan, S, workspace, O, st);
 }
 
 // ------------------------------------------------------------ K7 C ABI

@@ -137,6 +137,10 @@ struct OutP {
   int64_t ldo;
   int64_t* count;
   double eps;
+  // 0: sort + emit; 1: sort only (*count = merged terms, the (key, sum)
+  // entries stay in the workspace); 2: emit only, from a phase-1 workspace
+  int phase = 0;
+  int64_t capacity = INT64_MAX;  // output columns available (emit clamps)
 };
 
 __host__ __device__ inline int key_words_for_bits(int bits) {
@@ -1652,6 +1656,7 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S0, void* ws, const 
   const Dims D = to_dims(P);
   const Ctl C = to_ctl(P, ws);
   const WsLayout wl = ws_layout(P);
+  if (O.phase == 2) return launch_emit<W, KW>(L, D, C, O, st);
   PLB_CUDA(cudaMemsetAsync(ws, 0, (size_t)wl.leaf_desc, st));  // control region
 
   {

@@ -390,45 +390,131 @@ __device__ __noinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint8_t
 // the idle item buffer at the leaf's own offset, sums to C.sums -- plus the
 // leaf's kept count.  Leaves larger than the shared-memory capacity (one key
 // repeated more than leaf_cap times) are sorted in place in global memory.
-// Oversized leaf (one key repeated more than leaf_cap times): bitonic sort in
-// place in global memory, then tiles of kLeafThreads2*8 items.  Returns the
-// kept count (valid in thread 0).
-template <int W, int KW, int MODE>
-__device__ __noinline__ uint32_t leaf_sort_global(const Dims& D, const SrcA& S, const u64* GK,
-                                                  const uint32_t* GI, u64* DK, double2* DS,
-                                                  int n, double eps, uint32_t* s_warp) {
-  using RS = RunSum<W, KW, MODE>;
-  const int tid = threadIdx.x;
-    u64* K = const_cast<u64*>(GK);
-    uint32_t* I = const_cast<uint32_t*>(GI);
-    const int64_t stride = D.n;
-    bitonic_sort<KW>(K, I, stride, n);
-    const int tile = kLeafThreads2 * 8;
-    uint32_t base = 0;
-    for (int t0 = 0; t0 < n; t0 += tile) {
-      uint32_t mine = 0;
-      for (int p = t0 + tid * 8; p < min(n, t0 + tid * 8 + 8); ++p) {
-        if (p != 0 && key_eq<KW>(K, stride, p, p - 1)) continue;
-        int q = p + 1;
-        while (q < n && key_eq<KW>(K, stride, q, q - 1)) ++q;
-        if (keep_sum(RS::run(S, D.ma, I, p, q - p), eps)) ++mine;
-      }
-      uint32_t tt;
-      uint32_t pos = base + leaf_excl_scan(mine, s_warp, &tt);
-      for (int p = t0 + tid * 8; p < min(n, t0 + tid * 8 + 8); ++p) {
-        if (p != 0 && key_eq<KW>(K, stride, p, p - 1)) continue;
-        int q = p + 1;
-        while (q < n && key_eq<KW>(K, stride, q, q - 1)) ++q;
-        const double2 s = RS::run(S, D.ma, I, p, q - p);
-        if (keep_sum(s, eps)) {
+// Oversized leaf (a key repeated more than leaf_cap times, which no splitter
+// can divide), sorted by the CTA in global memory:
+//   1. tiles of `cap` items sorted in shared memory exactly like a normal leaf
+//      (radix window sort, bitonic fallback) and written back;
+//   2. merge passes over the sorted tiles (width cap, 2 cap, ...), ping-pong
+//      between the leaf's items and the idle buffer at the same offset: each
+//      thread takes an equal share of the output, finds its start by a
+//      merge-path binary search and merges sequentially;
+//   3. run heads, each run's end by binary search on the sorted keys, its sum
+//      (RunSum, numpy's order) computed once, |sum| <= eps dropped, kept
+//      (key, sum) compacted into the idle buffer / C.sums.
+// Round 1 used one global-memory bitonic network (H*H with |H| = 10^4: the
+// identity run of 10^4 items cost ~10 ms on one CTA).  Returns the kept count
+// (valid in thread 0).
+template <int KW>
+__device__ __forceinline__ bool item_lt2(const u64* K, const uint32_t* I, int64_t stride,
+                                         int64_t a, int64_t b) {
 #pragma unroll
-          for (int d = 0; d < KW; ++d) DK[d * stride + pos] = K[d * stride + p];
-          DS[pos] = s;
-          ++pos;
+  for (int d = 0; d < KW; ++d) {
+    const u64 ka = K[d * stride + a], kb = K[d * stride + b];
+    if (ka != kb) return ka < kb;
+  }
+  return I[a] < I[b];
+}
+
+template <int W, int KW, int MODE>
+__device__ __noinline__ uint32_t leaf_sort_global(const Dims& D, const SrcA& S, u64* K,
+                                                  uint32_t* I, u64* K2, uint32_t* I2,
+                                                  double2* DS, int n, double eps,
+                                                  uint32_t* s_warp, u64* SK, uint32_t* SI,
+                                                  uint8_t* scratch) {
+  using RS = RunSum<W, KW, MODE>;
+  constexpr int cap = leaf_cap_for(KW);
+  const int tid = threadIdx.x;
+  const int64_t stride = D.n;
+  // 1. sorted tiles
+  for (int t0 = 0; t0 < n; t0 += cap) {
+    const int m = min(cap, n - t0);
+    for (int t = tid; t < m; t += kLeafThreads2) {
+#pragma unroll
+      for (int d = 0; d < KW; ++d) SK[d * cap + t] = K[d * stride + t0 + t];
+      SI[t] = I[t0 + t];
+    }
+    __syncthreads();
+    if (m > 1 && !radix_sort_leaf<KW, cap>(SK, SI, m, scratch)) bitonic_sort_local<KW, cap>(SK, SI, m);
+    for (int t = tid; t < m; t += kLeafThreads2) {
+#pragma unroll
+      for (int d = 0; d < KW; ++d) K[d * stride + t0 + t] = SK[d * cap + t];
+      I[t0 + t] = SI[t];
+    }
+    __syncthreads();
+  }
+  // 2. merge passes
+  u64* sk = K;
+  uint32_t* si = I;
+  u64* dk = K2;
+  uint32_t* di = I2;
+  for (int w = cap; w < n; w *= 2) {
+    for (int a0 = 0; a0 < n; a0 += 2 * w) {
+      const int la = min(w, n - a0), lb = max(0, min(w, n - a0 - w));
+      const int64_t A = a0, B = a0 + la;
+      const int L = la + lb;
+      const int chunk = (L + kLeafThreads2 - 1) / kLeafThreads2;
+      const int d0 = min(L, tid * chunk), d1 = min(L, d0 + chunk);
+      if (d0 < d1) {
+        int lo = max(0, d0 - lb), hi = min(d0, la);  // A items before output d0
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (item_lt2<KW>(sk, si, stride, A + mid, B + (d0 - 1 - mid))) lo = mid + 1;
+          else hi = mid;
+        }
+        int i = lo, j = d0 - lo;
+        for (int o = d0; o < d1; ++o) {
+          const bool take_a = j >= lb || (i < la && item_lt2<KW>(sk, si, stride, A + i, B + j));
+          const int64_t src = take_a ? A + i++ : B + j++;
+#pragma unroll
+          for (int d = 0; d < KW; ++d) dk[d * stride + a0 + o] = sk[d * stride + src];
+          di[a0 + o] = si[src];
         }
       }
-      base += tt;
     }
+    __syncthreads();
+    u64* tk = sk; sk = dk; dk = tk;
+    uint32_t* ti = si; si = di; di = ti;
+  }
+  if (sk != K) {  // sorted data back into the leaf's own buffer
+    for (int t = tid; t < n; t += kLeafThreads2) {
+#pragma unroll
+      for (int d = 0; d < KW; ++d) K[d * stride + t] = sk[d * stride + t];
+      I[t] = si[t];
+    }
+    __syncthreads();
+  }
+  // 3. runs: sums once per head, compaction by tiles
+  const int tile = kLeafThreads2 * 8;
+  uint32_t base = 0;
+  for (int t0 = 0; t0 < n; t0 += tile) {
+    double2 sv[8];
+    uint32_t keepm = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int p = t0 + tid * 8 + u;
+      if (p >= n || (p != 0 && key_eq<KW>(K, stride, p, p - 1))) continue;
+      int lo = p + 1, hi = n;  // first position with a different (greater) key
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (key_eq<KW>(K, stride, mid, p)) lo = mid + 1;
+        else hi = mid;
+      }
+      sv[u] = RS::run(S, D.ma, I, p, lo - p);
+      if (keep_sum(sv[u], eps)) keepm |= 1u << u;
+    }
+    uint32_t tt;
+    uint32_t pos = base + leaf_excl_scan((uint32_t)__popc(keepm), s_warp, &tt);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (!(keepm >> u & 1)) continue;
+      const int p = t0 + tid * 8 + u;
+#pragma unroll
+      for (int d = 0; d < KW; ++d) K2[d * stride + pos] = K[d * stride + p];
+      DS[pos] = sv[u];
+      ++pos;
+    }
+    base += tt;
+  }
   return base;
 }
 
@@ -468,18 +554,20 @@ k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
   u64* DK = (dsc.x == 1 ? C.k2 : C.k1) + off;  // idle buffer at the same offset
   double2* DS = C.sums + off;
 
-  if (n > cap) {
-    const uint32_t kept = leaf_sort_global<W, KW, MODE>(D, S, GK, GI, DK, DS, n, eps, s_warp);
-    if (tid == 0) C.kept[leaf] = kept;
-    return;
-  }
-
   // shared memory: K [KW][cap] | I [cap] | POS u16 [cap] | HEAD u8 [cap] | scratch
   u64* K = sm;
   uint32_t* I = reinterpret_cast<uint32_t*>(K + (int64_t)KW * cap);
   uint16_t* POS = reinterpret_cast<uint16_t*>(I + cap);
   uint8_t* HEAD = reinterpret_cast<uint8_t*>(POS + cap);
   uint8_t* scratch = reinterpret_cast<uint8_t*>(sm) + leaf_buf_stride(KW);
+  if (n > cap) {
+    uint32_t* DI = (dsc.x == 1 ? C.i2 : C.i1) + off;
+    const uint32_t kept = leaf_sort_global<W, KW, MODE>(
+        D, S, const_cast<u64*>(GK), const_cast<uint32_t*>(GI), DK, DI, DS, n, eps, s_warp, K, I,
+        scratch);
+    if (tid == 0) C.kept[leaf] = kept;
+    return;
+  }
   double2* SUM = reinterpret_cast<double2*>(scratch);  // reuses the radix scratch
   for (int t = tid; t < n; t += kLeafThreads2) {
 #pragma unroll
@@ -636,8 +724,10 @@ k_emit(Layout L, Dims D, Ctl C, OutP O) {
   uint8_t* ZB = reinterpret_cast<uint8_t*>(PB + 2 * T);      // [T] zero phase bytes
   const int tid = threadIdx.x;
   const uint32_t n_leaves = *C.n_leaves;
-  const uint32_t total = *C.scan_total;
-  if (blockIdx.x == 0 && tid == 0) *O.count = (int64_t)total;
+  const uint32_t total_all = *C.scan_total;
+  if (blockIdx.x == 0 && tid == 0) *O.count = (int64_t)total_all;
+  // never write past the caller's columns (phase 2 sizes them from phase 1)
+  const uint32_t total = (int64_t)total_all < O.capacity ? total_all : (uint32_t)O.capacity;
   for (int e = tid; e < T; e += kEmitThreads) ZB[e] = 0;
   fence_async_smem();
   // full tiles go out through TMA bulk stores when every destination is
@@ -746,6 +836,10 @@ k_emit(Layout L, Dims D, Ctl C, OutP O) {
   if (tid == 0) bulk_wait_all();
 }
 
+template <int W, int KW>
+static int launch_emit(const Layout& L, const Dims& D, const Ctl& C, const OutP& O,
+                       cudaStream_t st);
+
 template <int W, int KW, int MODE>
 static int launch_leaves(const Layout& L, const Dims& D, const SrcA& S, const Ctl& C,
                          const OutP& O, cudaStream_t st) {
@@ -768,6 +862,16 @@ static int launch_leaves(const Layout& L, const Dims& D, const SrcA& S, const Ct
     k_range_map<KW><<<(unsigned)ceil_div(D.max_leaves, 256), 256, 0, st>>>(D, C);
     PLB_CHECK_LAUNCH("k_range_map");
   }
+  if (O.phase == 1) {  // merged count only (count's high word was zeroed by k_buckets)
+    PLB_CUDA(cudaMemcpyAsync(O.count, C.scan_total, 4, cudaMemcpyDeviceToDevice, st));
+    return PL_OK;
+  }
+  return launch_emit<W, KW>(L, D, C, O, st);
+}
+
+template <int W, int KW>
+static int launch_emit(const Layout& L, const Dims& D, const Ctl& C, const OutP& O,
+                       cudaStream_t st) {
   const size_t esm = emit_smem_bytes(KW);
   auto ke = k_emit<W, KW>;
   if (esm > 48 * 1024)

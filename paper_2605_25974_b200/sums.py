@@ -490,6 +490,22 @@ def _new_sum(n, x, z, k, c) -> PauliSumSoA:
     return out
 
 
+# Merges with more raw items than this run in two phases (merge + count, then
+# emit into planes of exactly the merged size): no raw-size output buffers.
+# Smaller merges emit into raw-size planes in the same call (no host sync
+# between the phases) and are right-sized by _fitted.
+_TWO_PHASE_MIN = 1 << 22
+
+
+def _emit_exact(n, plan, ws, W: int, m: int, dev, st) -> PauliSumSoA:
+    x, z, k, c = _alloc_planes(W, m, dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    if m:
+        _native.call("pl_merge_emit", C.byref(plan), ptr(ws), ws.numel(), ptr(x), ptr(z), ptr(k),
+                     ptr(c), x.stride(0), m, ptr(cnt), st)
+    return _new_sum(n, x[:, :m], z[:, :m], k[:m], c[:m])
+
+
 def _fitted(n, x, z, k, c, m: int) -> PauliSumSoA:
     """The first m merged terms of capacity-sized output planes.  Views are
     kept while they waste at most half the allocation; a heavily merged
@@ -537,14 +553,19 @@ def outer_multiply(a: PauliSumSoA, b: PauliSumSoA, *, eps: float = 0.0, combine:
                          ptr(B.z), B.ld, C.byref(plan), st)
             _remember(plan)
             ws = torch.empty(max(int(plan.workspace_bytes), 1), dtype=torch.uint8, device=dev)
-            x, z, k, c = _alloc_planes(W, n_items, dev)
             cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-            _native.call("pl_outer_multiply_combine", C.byref(plan),
-                         ptr(A.x), ptr(A.z), ptr(A.k), ptr(A.c), A.ld,
-                         ptr(B.x), ptr(B.z), ptr(B.k), ptr(B.c), B.ld,
-                         float(eps), ptr(ws), ws.numel(),
-                         ptr(x), ptr(z), ptr(k), ptr(c), x.stride(0), ptr(cnt), st)
-            out = _fitted(a.n, x, z, k, c, int(cnt.item()))
+            args = (ptr(A.x), ptr(A.z), ptr(A.k), ptr(A.c), A.ld,
+                    ptr(B.x), ptr(B.z), ptr(B.k), ptr(B.c), B.ld, float(eps), ptr(ws), ws.numel())
+            if n_items > _TWO_PHASE_MIN:
+                # merge, read the merged count, then emit into exactly sized planes
+                _native.call("pl_outer_multiply_combine", C.byref(plan), *args,
+                             None, None, None, None, 0, ptr(cnt), st)
+                out = _emit_exact(a.n, plan, ws, W, int(cnt.item()), dev, st)
+            else:
+                x, z, k, c = _alloc_planes(W, n_items, dev)
+                _native.call("pl_outer_multiply_combine", C.byref(plan), *args,
+                             ptr(x), ptr(z), ptr(k), ptr(c), x.stride(0), ptr(cnt), st)
+                out = _fitted(a.n, x, z, k, c, int(cnt.item()))
     return _download(out) if back else out
 
 
@@ -564,12 +585,17 @@ def sort_combine(s: PauliSumSoA, *, eps: float = 0.0) -> PauliSumSoA:
             _native.call("pl_sort_plan", W, m, ptr(S.x), ptr(S.z), S.ld, C.byref(plan), st)
             _remember(plan)
             ws = torch.empty(max(int(plan.workspace_bytes), 1), dtype=torch.uint8, device=dev)
-            x, z, k, c = _alloc_planes(W, m, dev)
             cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-            _native.call("pl_sort_combine", C.byref(plan), ptr(S.x), ptr(S.z), ptr(S.k),
-                         ptr(S.c), S.ld, float(eps), ptr(ws), ws.numel(),
-                         ptr(x), ptr(z), ptr(k), ptr(c), x.stride(0), ptr(cnt), st)
-            out = _fitted(s.n, x, z, k, c, int(cnt.item()))
+            args = (ptr(S.x), ptr(S.z), ptr(S.k), ptr(S.c), S.ld, float(eps), ptr(ws), ws.numel())
+            if m > _TWO_PHASE_MIN:
+                _native.call("pl_sort_combine", C.byref(plan), *args, None, None, None, None, 0,
+                             ptr(cnt), st)
+                out = _emit_exact(s.n, plan, ws, W, int(cnt.item()), dev, st)
+            else:
+                x, z, k, c = _alloc_planes(W, m, dev)
+                _native.call("pl_sort_combine", C.byref(plan), *args,
+                             ptr(x), ptr(z), ptr(k), ptr(c), x.stride(0), ptr(cnt), st)
+                out = _fitted(s.n, x, z, k, c, int(cnt.item()))
     return _download(out) if back else out
 
 

@@ -357,3 +357,20 @@ def test_sampler_constant_leading_key_word(cuda):
     gx, gz, gk, gc = got.columns()
     assert np.array_equal(gx, ex) and np.array_equal(gz, ez)
     assert np.abs(gc - ec).max(initial=0) <= 1e-12 * np.abs(ec).sum()
+
+
+def test_two_phase_exact_emit_equals_single_call(cuda, monkeypatch):
+    """Large merges run as merge + count, then pl_merge_emit into exactly sized
+    planes; forcing that path on small inputs gives the same sums."""
+    a, b = rng.config_columns(2, 0.3)
+    A, B = soa(500, a, cuda), soa(500, b, cuda)
+    h = rng.local_columns(64, 800, rng.SplitMix64(3), 12, (1, 3))
+    H = soa(64, h, cuda)
+    x, z, f, c = rng.c5_columns(20_000, seed=9)
+    S = soa(500, (x, z, f, c), cuda)
+    ref = [pl.outer_multiply(A, B), H * H, pl.sort_and_combine(S)]
+    monkeypatch.setattr(pl.sums, "_TWO_PHASE_MIN", 0)
+    got = [pl.outer_multiply(A, B), H * H, pl.sort_and_combine(S)]
+    for r, g in zip(ref, got):
+        assert g == r
+        assert g.x.shape[1] == len(g)  # exactly sized planes
