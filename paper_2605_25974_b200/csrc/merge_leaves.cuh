@@ -212,12 +212,36 @@ __device__ __forceinline__ uint32_t key_window(const u64* K, int stride, int t, 
   return (uint32_t)(v >> (64 - kRadixWindow));
 }
 
+// (key, ik) order of items a, b of a tie segment; *dup set when the keys are equal
+template <int KW>
+__device__ __forceinline__ bool item_lt_dup(const u64* K, const uint32_t* I, int stride, int a,
+                                            int b, int* dup) {
+#pragma unroll
+  for (int d = 0; d < KW; ++d) {
+    const u64 ka = K[d * stride + a], kb = K[d * stride + b];
+    if (ka != kb) return ka < kb;
+  }
+  *dup = 1;
+  return I[a] < I[b];
+}
+
+// Result of radix_rank_leaf
+constexpr int kRankFallback = 0;  // no order produced (equal keys / long window ties)
+constexpr int kRankDistinct = 1;  // *perm holds the order, every key differs
+constexpr int kRankDups = 2;      // *perm holds the order, some keys are equal
+
+// Ranks the n items of a leaf by (key, ik) without moving them: (*perm)[t] is
+// the position of the item of rank t.  The first pass takes its window keys
+// straight from the leaf's keys (no staging pass), per-warp bin counters are
+// read and written as packed pairs, and the block scan alternates between two
+// warp-total buffers (four barriers per pass).
 template <int KW, int CAP>
-__device__ __noinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint8_t* scratch) {
+__device__ __noinline__ int radix_rank_leaf(const u64* K, const uint32_t* I, int n,
+                                            uint8_t* scratch, uint16_t** perm) {
   static_assert(CAP % kLeafThreads2 == 0, "leaf capacity must be a multiple of the CTA size");
   constexpr int SEG = CAP / kLeafWarps2;             // max positions owned by one warp
   constexpr int SLOTS = SEG >= 32 ? SEG / 32 : 1;
-  // only the first npos positions take part: warps own seg = npos / 8 each
+  // only the first npos positions take part: warps own seg = npos / 4 each
   const int npos = SEG >= 32 ? (n + kLeafThreads2 - 1) / kLeafThreads2 * kLeafThreads2 : CAP;
   const int seg = SEG >= 32 ? npos / kLeafWarps2 : SEG;
   const int slots = SEG >= 32 ? seg / 32 : 1;
@@ -227,8 +251,8 @@ __device__ __noinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint8_t
                      reinterpret_cast<uint16_t*>(scratch + 8 * CAP) + CAP};
   uint16_t* hist = reinterpret_cast<uint16_t*>(scratch + 12 * CAP);  // [warp][bin]
   __shared__ u64 s_or[kLeafWarps2][KW];
-  __shared__ int s_flag;
-  __shared__ uint32_t s_scan[kLeafWarps2];
+  __shared__ int s_flag, s_dup;
+  __shared__ uint32_t s_scan[2][kLeafWarps2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   // 1. highest bit at which any key differs from item 0
@@ -245,7 +269,10 @@ __device__ __noinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint8_t
     for (int o = 16; o > 0; o >>= 1) acc[d] |= __shfl_xor_sync(0xffffffffu, acc[d], o);
     if (lane == 0) s_or[warp][d] = acc[d];
   }
-  if (tid == 0) s_flag = 0;
+  if (tid == 0) {
+    s_flag = 0;
+    s_dup = 0;
+  }
   __syncthreads();
   int p = -1;
 #pragma unroll
@@ -255,24 +282,22 @@ __device__ __noinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint8_t
     for (int w = 0; w < kLeafWarps2; ++w) v |= s_or[w][d];
     if (v) p = d * 64 + __clzll(v);
   }
-  if (p < 0) return false;  // every key equal: order is by ik alone (bitonic)
+  if (p < 0) return kRankFallback;  // every key equal: order is by ik alone (bitonic)
 
-  // 2. window keys in position order; positions >= n sort last (stable, max key)
-  for (int t = tid; t < npos; t += kLeafThreads2) {
-    wk[0][t] = t < n ? key_window<KW>(K, CAP, t, p) : 0xFFFFFFFFu >> (32 - kRadixWindow);
-    wp[0][t] = (uint16_t)t;
-  }
-  __syncthreads();
-
-  // 3. LSD passes; warp w owns positions [w*seg, (w+1)*seg), slot-major
+  // 2. LSD passes; warp w owns positions [w*seg, (w+1)*seg), slot-major.
+  //    Positions >= n carry the maximal window and sort last (stable).
   const unsigned lt_mask = (1u << lane) - 1u;
   const bool lane_on = SEG >= 32 || lane < SEG;
+  const unsigned wmask = SEG >= 32 ? 0xffffffffu : ((1u << SEG) - 1u);
   int cur = 0;
 #pragma unroll 1
   for (int pass = 0; pass < kRadixPasses; ++pass) {
     const int sh = pass * kRadixBits;
     uint16_t* hw = hist + warp * kRadixBins;
-    for (int b = lane; b < kRadixBins; b += 32) hw[b] = 0;
+    {
+      uint32_t* hz = reinterpret_cast<uint32_t*>(hw);
+      for (int b = lane; b < kRadixBins / 2; b += 32) hz[b] = 0u;
+    }
     __syncwarp();
     uint32_t key[SLOTS];
     uint16_t pm[SLOTS], rk[SLOTS];
@@ -280,39 +305,57 @@ __device__ __noinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint8_t
     for (int s = 0; s < SLOTS; ++s) {
       const int pos = warp * seg + s * 32 + lane;
       if (lane_on && s < slots) {
-        key[s] = wk[cur][pos];
-        pm[s] = wp[cur][pos];
+        if (pass == 0) {
+          key[s] = pos < n ? key_window<KW>(K, CAP, pos, p) : 0xFFFFFFFFu >> (32 - kRadixWindow);
+          pm[s] = (uint16_t)pos;
+        } else {
+          key[s] = wk[cur][pos];
+          pm[s] = wp[cur][pos];
+        }
         const uint32_t dg = (key[s] >> sh) & (kRadixBins - 1);
-        const unsigned grp = __match_any_sync(SEG >= 32 ? 0xffffffffu : ((1u << SEG) - 1u), dg);
+        const unsigned grp = __match_any_sync(wmask, dg);
         const uint16_t prev = hw[dg];
-        __syncwarp(SEG >= 32 ? 0xffffffffu : ((1u << SEG) - 1u));
+        __syncwarp(wmask);
         if ((grp & lt_mask) == 0) hw[dg] = (uint16_t)(prev + __popc(grp));
-        __syncwarp(SEG >= 32 ? 0xffffffffu : ((1u << SEG) - 1u));
+        __syncwarp(wmask);
         rk[s] = (uint16_t)(prev + __popc(grp & lt_mask));
       }
     }
     __syncthreads();
     // bin-major offsets: bin b's start, then warps in order inside the bin;
-    // thread t owns the BPT consecutive bins [t*BPT, (t+1)*BPT)
+    // thread t owns the adjacent bins 2t, 2t+1 (one packed word per warp)
     {
-      constexpr int BPT = kRadixBins / kLeafThreads2;
-      static_assert(BPT >= 1 && BPT * kLeafThreads2 == kRadixBins, "bins per thread");
+      static_assert(kRadixBins == 2 * kLeafThreads2, "two bins per thread");
+      uint32_t* h32 = reinterpret_cast<uint32_t*>(hist);
+      uint32_t c[kLeafWarps2];
       uint32_t tot = 0;
 #pragma unroll
-      for (int i = 0; i < BPT; ++i)
+      for (int w = 0; w < kLeafWarps2; ++w) {
+        c[w] = h32[w * (kRadixBins / 2) + tid];
+        tot += (c[w] & 0xFFFFu) + (c[w] >> 16);
+      }
+      uint32_t inc = tot;
 #pragma unroll
-        for (int w = 0; w < kLeafWarps2; ++w) tot += hist[w * kRadixBins + tid * BPT + i];
-      uint32_t all;
-      uint32_t run = leaf_excl_scan(tot, s_scan, &all);
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      uint32_t* sc = s_scan[pass & 1];
+      if (lane == 31) sc[warp] = inc;
+      __syncthreads();
+      uint32_t run = inc - tot;
 #pragma unroll
-      for (int i = 0; i < BPT; ++i) {
+      for (int w = 0; w < kLeafWarps2; ++w) run += w < warp ? sc[w] : 0u;
+      uint32_t lo_off[kLeafWarps2];
 #pragma unroll
-        for (int w = 0; w < kLeafWarps2; ++w) {
-          const int h = w * kRadixBins + tid * BPT + i;
-          const uint16_t c = hist[h];
-          hist[h] = (uint16_t)run;
-          run += c;
-        }
+      for (int w = 0; w < kLeafWarps2; ++w) {
+        lo_off[w] = run;
+        run += c[w] & 0xFFFFu;
+      }
+#pragma unroll
+      for (int w = 0; w < kLeafWarps2; ++w) {
+        h32[w * (kRadixBins / 2) + tid] = lo_off[w] | (run << 16);
+        run += c[w] >> 16;
       }
     }
     __syncthreads();
@@ -330,7 +373,7 @@ __device__ __noinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint8_t
     __syncthreads();
   }
 
-  // 4. finish segments of equal windows on the full (key, ik)
+  // 3. finish segments of equal windows on the full (key, ik)
   const uint32_t* sk = wk[cur];
   uint16_t* sp = wp[cur];
   for (int q = tid; q < n; q += kLeafThreads2) {
@@ -341,20 +384,28 @@ __device__ __noinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint8_t
       s_flag = 1;
       continue;
     }
+    int dup = 0;
     for (int a = q + 1; a < e; ++a) {  // insertion sort of sp[q..e)
       const uint16_t v = sp[a];
       int b = a;
-      while (b > q && item_lt<KW>(K, I, CAP, v, sp[b - 1])) {
+      while (b > q && item_lt_dup<KW>(K, I, CAP, v, sp[b - 1], &dup)) {
         sp[b] = sp[b - 1];
         --b;
       }
       sp[b] = v;
     }
+    if (dup) s_dup = 1;
   }
   __syncthreads();
-  if (s_flag) return false;
+  if (s_flag) return kRankFallback;
+  *perm = sp;
+  return s_dup ? kRankDups : kRankDistinct;
+}
 
-  // 5. gather K, I into sorted order in place
+// Moves K, I into the order perm[0..n) in place (perm[t] = source of rank t).
+template <int KW, int CAP>
+__device__ __forceinline__ void apply_leaf_perm(u64* K, uint32_t* I, int n, const uint16_t* sp) {
+  const int tid = threadIdx.x;
   constexpr int PER = (CAP + kLeafThreads2 - 1) / kLeafThreads2;
   u64 gk[PER][KW];
   uint32_t gi[PER];
@@ -379,6 +430,14 @@ __device__ __noinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint8_t
     }
   }
   __syncthreads();
+}
+
+// Sorts the leaf in place; false = not sorted (the caller runs the bitonic network).
+template <int KW, int CAP>
+__device__ __forceinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint8_t* scratch) {
+  uint16_t* sp = nullptr;
+  if (radix_rank_leaf<KW, CAP>(K, I, n, scratch, &sp) == kRankFallback) return false;
+  apply_leaf_perm<KW, CAP>(K, I, n, sp);
   return true;
 }
 
@@ -576,7 +635,42 @@ k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
   }
   __syncthreads();
   LEAF_T(1);
-  if (n > 1 && !radix_sort_leaf<KW, cap>(K, I, n, scratch)) bitonic_sort_local<KW, cap>(K, I, n);
+  if (n > 1) {
+    uint16_t* sp = nullptr;
+    const int rank = radix_rank_leaf<KW, cap>(K, I, n, scratch, &sp);
+    if (rank == kRankDistinct) {
+      // Every key of the leaf differs: each item is its own run, so nothing is
+      // moved in shared memory -- rank t's key and coefficient go straight to
+      // the leaf's output slots (kept = n) unless a coefficient is dropped.
+      constexpr int PERF = cap / kLeafThreads2;
+      double2 cf[PERF];
+      int src[PERF];
+      bool drop = false;
+#pragma unroll
+      for (int r = 0; r < PERF; ++r) {
+        const int t = r * kLeafThreads2 + tid;
+        src[r] = t < n ? (int)sp[t] : -1;
+        if (t < n) cf[r] = Source<W, KW, MODE>::coef(S, D.ma, I[src[r]]);
+      }
+#pragma unroll
+      for (int r = 0; r < PERF; ++r)
+        if (src[r] >= 0 && !keep_sum(cf[r], eps)) drop = true;
+      if (!__syncthreads_or(drop)) {
+#pragma unroll
+        for (int r = 0; r < PERF; ++r) {
+          const int t = r * kLeafThreads2 + tid;
+          if (src[r] < 0) continue;
+#pragma unroll
+          for (int d = 0; d < KW; ++d) DK[d * D.n + t] = K[d * cap + src[r]];
+          DS[t] = cf[r];
+        }
+        if (tid == 0) C.kept[leaf] = (uint32_t)n;
+        return;
+      }
+    }
+    if (rank == kRankFallback) bitonic_sort_local<KW, cap>(K, I, n);
+    else apply_leaf_perm<KW, cap>(K, I, n, sp);
+  }
   LEAF_T(2);
   for (int p = tid; p < n; p += kLeafThreads2)
     HEAD[p] = (p == 0 || !key_eq<KW>(K, cap, p, p - 1)) ? 1 : 0;
