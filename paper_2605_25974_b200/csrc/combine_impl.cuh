@@ -83,6 +83,10 @@ struct Ctl {  // control arrays inside the workspace
   uint32_t* leaf_ctr;    // 1
   uint4* leaf_desc;      // max_leaves: (buffer 1|2, offset, size, 0)
   u64* split2;           // [nb1][KW][max_sub] level-2 splitters per bucket
+  u64* split2w;          // [nb1][max_sub] 64-bit window of each level-2 splitter (after bcp bits)
+  int32_t* bcp;          // nb1: bits shared by every key of the bucket (window offset)
+  uint16_t* bid;         // level-1 bucket of every generated item (k_count -> k_scatter)
+  uint16_t* sid;         // [n] level-2 sub-bucket of every item (k_split_count -> k_split_scatter)
   uint32_t* sub_count;   // [nb1][max_sub] level-2 counts, then cursors
   uint32_t* tile_off;    // nb1 + 1: first split tile of each bucket
   uint32_t* n_tiles;     // 1
@@ -731,11 +735,12 @@ struct GenSmem {
   uint16_t* tab;   // level-1 prefix table (2^kTabBits + 1)
 };
 
+// search = false (k_scatter): no splitters and no prefix table
 template <int W>
-__device__ __forceinline__ GenSmem gen_smem(u64* sm, int nb1, int KW) {
+__device__ __forceinline__ GenSmem gen_smem(u64* sm, int nb1, int KW, bool search = true) {
   GenSmem g;
   g.split = sm;
-  g.hist = reinterpret_cast<uint32_t*>(sm + (int64_t)KW * nb1);
+  g.hist = reinterpret_cast<uint32_t*>(sm + (search ? (int64_t)KW * nb1 : 0));
   g.gbase = g.hist + nb1;
   g.tile = reinterpret_cast<u64*>(g.gbase + nb1);  // 2*nb1 u32 keeps 8-byte alignment
   g.tkey = g.tile + 2 * W * kTileB;
@@ -746,10 +751,10 @@ __device__ __forceinline__ GenSmem gen_smem(u64* sm, int nb1, int KW) {
   return g;
 }
 
-__host__ __device__ constexpr size_t gen_smem_bytes(int W, int KW, int nb1) {
-  return (size_t)8 * KW * nb1 + 8 * (size_t)nb1 + (size_t)16 * W * kTileB +
+__host__ __device__ constexpr size_t gen_smem_bytes(int W, int KW, int nb1, bool search = true) {
+  return (search ? (size_t)8 * KW * nb1 : 0) + 8 * (size_t)nb1 + 8 + (size_t)16 * W * kTileB +
          (size_t)8 * KW * kTileB + 8 * (size_t)kTileB + (size_t)4 * kGenTB * kGenThreads +
-         2 * (size_t)((1 << kTabBits) + 1) + 64;
+         (search ? 2 * (size_t)((1 << kTabBits) + 1) : 0) + 64;
 }
 
 template <int KW>
@@ -822,6 +827,20 @@ struct Gen {
       for (int d = 0; d < KW; ++d) ka[d] = valid_i ? C.opk[d * nops + i] : 0ull;
       pa = valid_i ? C.opb[i] : 0;
     }
+  }
+
+  // whether item jj of this thread exists (no loads)
+  __device__ __forceinline__ bool valid(const Dims& D, int jj) const {
+    if (MODE == 0) {
+      const int bb = (threadIdx.x / kTileA) * kGenTB + jj;
+      return valid_i && (int64_t)blockIdx.y * kTileB + bb < D.mb;
+    }
+    return (int64_t)blockIdx.x * blockDim.x * kGenTB + (int64_t)jj * blockDim.x + threadIdx.x < D.n;
+  }
+  // slot of item jj in the per-item bucket-id array (coalesced over threads)
+  static __device__ __forceinline__ int64_t slot_of(int jj) {
+    const int64_t blk = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+    return (blk * kGenTB + jj) * kGenThreads + threadIdx.x;
   }
 
   // item jj of this thread: returns false when out of range
@@ -942,6 +961,10 @@ k_count(Layout L, Dims D, SrcA S, Ctl C) {
         }
       }
     }
+    // the bucket of every item is kept for k_scatter (no second search)
+#pragma unroll
+    for (int u = 0; u < kGenIlp; ++u)
+      C.bid[Gen<W, KW, MODE>::slot_of(j0 + u)] = (uint16_t)pos[u];
     // warp-aggregated histogram: a tile's items share few buckets
 #pragma unroll
     for (int u = 0; u < kGenIlp; ++u) {
@@ -958,62 +981,37 @@ k_count(Layout L, Dims D, SrcA S, Ctl C) {
 }
 
 template <int W, int KW, int MODE>
-__global__ void __launch_bounds__(kGenThreads, 3)
+__global__ void __launch_bounds__(kGenThreads, W <= 8 ? 4 : 3)
 k_scatter(Layout L, Dims D, SrcA S, Ctl C) {
   extern __shared__ u64 sm[];
-  const GenSmem g = gen_smem<W>(sm, D.nb1, KW);
-  gen_prologue<KW>(g, C, D.nb1);
+  const GenSmem g = gen_smem<W>(sm, D.nb1, KW, false);
+  for (int b = threadIdx.x; b < D.nb1; b += blockDim.x) g.hist[b] = 0;
   Gen<W, KW, MODE> gen;
   gen.init(L, D, S, C, g);
   __syncthreads();
-#pragma unroll 1
-  for (int j0 = 0; j0 < kGenTB; j0 += kGenIlp) {
-    u64 key[kGenIlp][KW];
-    bool ok[kGenIlp];
-    int pos[kGenIlp];
+  // bucket ids come from k_count (a single bucket needs none); lanes with the
+  // same bucket get consecutive slots (warp-aggregated ranks)
+  const bool one = D.nb1 == 1;
+  const int lane = threadIdx.x & 31;
+  uint16_t bids[kGenTB];  // all id loads in flight together
 #pragma unroll
-    for (int u = 0; u < kGenIlp; ++u) {
-      uint32_t ik;
-      ok[u] = gen.item(L, D, C, g, j0 + u, key[u], ik);
-      pos[u] = 0;
-    }
-    // the prefix table narrows each search to the splitters sharing the
-    // key's top kTabBits bits (usually none or a few)
-    int hi[kGenIlp], step[kGenIlp];
-    int smax = 0;
+  for (int jj = 0; jj < kGenTB; ++jj)
+    bids[jj] = (!one && gen.valid(D, jj)) ? C.bid[Gen<W, KW, MODE>::slot_of(jj)] : (uint16_t)0;
 #pragma unroll
-    for (int u = 0; u < kGenIlp; ++u) {
-      const int h = (int)(key[u][0] >> (64 - kTabBits));
-      pos[u] = g.tab[h];
-      hi[u] = g.tab[h + 1];
-      step[u] = pow2_floor(hi[u] - pos[u]);
-      smax = step[u] > smax ? step[u] : smax;
+  for (int jj = 0; jj < kGenTB; ++jj) {
+    const bool ok = gen.valid(D, jj);
+    const int pos = bids[jj];
+    uint32_t code = 0xFFFFFFFFu;
+    const unsigned act = __ballot_sync(0xffffffffu, ok);
+    if (ok) {
+      const unsigned peers = __match_any_sync(act, pos);
+      const int leader = __ffs(peers) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(&g.hist[pos], (uint32_t)__popc(peers));
+      base = __shfl_sync(peers, base, leader);
+      code = ((uint32_t)pos << 16) | (base + __popc(peers & ((1u << lane) - 1u)));
     }
-    for (int st = smax; st > 0; st >>= 1) {
-#pragma unroll
-      for (int u = 0; u < kGenIlp; ++u) {
-        if (step[u] >= st) {
-          const int c = pos[u] + st;
-          if (c <= hi[u] && !key_lt<KW>(key[u], g.split, D.nb1, c - 1)) pos[u] = c;
-        }
-      }
-    }
-    // warp-aggregated ranks: lanes with the same bucket get consecutive slots
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int u = 0; u < kGenIlp; ++u) {
-      uint32_t code = 0xFFFFFFFFu;
-      const unsigned act = __ballot_sync(0xffffffffu, ok[u]);
-      if (ok[u]) {
-        const unsigned peers = __match_any_sync(act, pos[u]);
-        const int leader = __ffs(peers) - 1;
-        uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(&g.hist[pos[u]], (uint32_t)__popc(peers));
-        base = __shfl_sync(peers, base, leader);
-        code = ((uint32_t)pos[u] << 16) | (base + __popc(peers & ((1u << lane) - 1u)));
-      }
-      g.slot[(j0 + u) * kGenThreads + threadIdx.x] = code;
-    }
+    g.slot[jj * kGenThreads + threadIdx.x] = code;
   }
   __syncthreads();
   for (int b = threadIdx.x; b < D.nb1; b += blockDim.x)
@@ -1175,21 +1173,37 @@ k_split_prep(Dims D, Ctl C, int s2cap) {
   __syncthreads();
   const bool composite = sort_samples<KW>(SK, ns, CK, cp);
   u64* SP = C.split2 + (int64_t)b * KW * D.max_sub;
+  u64* SPW = C.split2w + (int64_t)b * D.max_sub;
+  if (threadIdx.x == 0) C.bcp[b] = cp;
   for (int q = 1 + threadIdx.x; q < nsub; q += blockDim.x) {
     const int pos = (int)(((int64_t)q * ns) / nsub);
     const int src = composite ? (int)(CK[pos] & 0x1FFF) : pos;
+    u64 key[KW];
 #pragma unroll
-    for (int d = 0; d < KW; ++d) SP[d * D.max_sub + (q - 1)] = SK[d * ns + src];
+    for (int d = 0; d < KW; ++d) {
+      key[d] = SK[d * ns + src];
+      SP[d * D.max_sub + (q - 1)] = key[d];
+    }
+    SPW[q - 1] = get_seg<KW>(key, cp, 64);  // the 64 key bits after the bucket's shared prefix
   }
 }
 
-// tile t -> its bucket (last b with tile_off[b] <= t)
-__device__ __forceinline__ int tile_bucket(const Ctl& C, int nb1, uint32_t t) {
-  int lo = 0, hi = nb1 - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (C.tile_off[mid] <= t) lo = mid;
-    else hi = mid - 1;
+// tile t -> its bucket (last b with tile_off[b] <= t; tile_off non-decreasing,
+// tile_off[0] == 0).  Warp-cooperative 32-ary search: every round the lanes
+// probe 32 evenly spaced entries of the current range at once, so nb1 <= 1024
+// takes two rounds of one load each instead of ten dependent loads.
+__device__ __forceinline__ int tile_bucket_warp(const Ctl& C, int nb1, uint32_t t) {
+  const int lane = threadIdx.x & 31;
+  int lo = 0, len = nb1;  // answer in [lo, lo + len)
+  while (len > 1) {
+    const int step = (len + 31) / 32;
+    const int idx = lo + lane * step;
+    const bool le = idx < lo + len && C.tile_off[idx] <= t;
+    const unsigned m = __ballot_sync(0xffffffffu, le);  // lane 0 always set
+    const int hi_lane = 31 - __clz((int)m);
+    const int nlo = lo + hi_lane * step;
+    len = min(step, lo + len - nlo);
+    lo = nlo;
   }
   return lo;
 }
@@ -1199,14 +1213,17 @@ struct SplitTile {
   uint32_t base, size, t0, t1;  // bucket base/size; item range [t0, t1) inside the bucket
 };
 
-// loads the tile's bucket splitters into shared memory; false if no tile
-template <int KW>
-__device__ __forceinline__ bool split_tile_setup(const Dims& D, const Ctl& C, u64* SP,
-                                                 uint32_t* hist, SplitTile& T) {
+// Locates the CTA's tile (bucket, item range) and clears the tile histogram;
+// false if the grid has no such tile.
+__device__ __forceinline__ bool split_tile_setup(const Dims& D, const Ctl& C, uint32_t* hist,
+                                                 SplitTile& T) {
   __shared__ int s_b;
   const uint32_t t = blockIdx.x;
   if (t >= *C.n_tiles) return false;
-  if (threadIdx.x == 0) s_b = tile_bucket(C, D.nb1, t);
+  if (threadIdx.x < 32) {
+    const int b = tile_bucket_warp(C, D.nb1, t);
+    if (threadIdx.x == 0) s_b = b;
+  }
   __syncthreads();
   T.b = s_b;
   T.base = C.bbase[T.b];
@@ -1214,31 +1231,72 @@ __device__ __forceinline__ bool split_tile_setup(const Dims& D, const Ctl& C, u6
   T.nsub = leaves_for(T.size, D);
   T.t0 = (t - C.tile_off[T.b]) * kSplitTile;
   T.t1 = min(T.size, T.t0 + kSplitTile);
-  const u64* G = C.split2 + (int64_t)T.b * KW * D.max_sub;
-  for (int q = threadIdx.x; q < T.nsub; q += blockDim.x) {
-    hist[q] = 0;
-    if (q < T.nsub - 1) {
-#pragma unroll
-      for (int d = 0; d < KW; ++d) SP[d * D.max_sub + q] = G[d * D.max_sub + q];
-    }
-  }
-  __syncthreads();
+  for (int q = threadIdx.x; q < T.nsub; q += blockDim.x) hist[q] = 0;
   return true;
 }
 
+constexpr int kSplitIpt = kSplitTile / kSplitTileThreads;  // items per thread
+constexpr int kSplitWinSlots = 1024;                        // padded window table (>= max_sub)
+
+// Level-2 classification searches 32-bit windows: the key bits after the
+// prefix every key of the bucket shares (C.bcp) -- one shared-memory word and
+// one compare per step of a fixed ten-step search over a table padded with
+// the maximal window, a thread's items interleaved.  Splitters whose window
+// equals the key's (rare) are compared in full from global memory.  Every
+// item's sub-bucket goes to C.sid, so k_split_scatter does not search again.
 template <int KW>
 __global__ void __launch_bounds__(kSplitTileThreads)
 k_split_count(Dims D, Ctl C) {
   extern __shared__ u64 sm[];
-  u64* SP = sm;
-  uint32_t* hist = reinterpret_cast<uint32_t*>(SP + (int64_t)KW * D.max_sub);
+  uint32_t* SPW = reinterpret_cast<uint32_t*>(sm);  // [kSplitWinSlots] splitter windows
+  uint32_t* hist = SPW + kSplitWinSlots;
   SplitTile T;
-  if (!split_tile_setup<KW>(D, C, SP, hist, T)) return;
+  if (!split_tile_setup(D, C, hist, T)) return;
+  const int nsp = T.nsub - 1;
+  {
+    const u64* G = C.split2w + (int64_t)T.b * D.max_sub;
+    for (int q = threadIdx.x; q < kSplitWinSlots; q += blockDim.x)
+      SPW[q] = q < nsp ? (uint32_t)(G[q] >> 32) : 0xFFFFFFFFu;
+  }
+  const int cp = C.bcp[T.b];
   const u64* K1 = C.k1 + T.base;
-  for (uint32_t t = T.t0 + threadIdx.x; t < T.t1; t += kSplitTileThreads) {
-    u64 key[KW];
-    load_key<KW>(K1, D.n, t, key);
-    atomicAdd(&hist[bucket_of<KW>(key, SP, D.max_sub, T.nsub - 1)], 1u);
+  const u64* SPF = C.split2 + (int64_t)T.b * KW * D.max_sub;
+  uint16_t* SID = C.sid + T.base;
+  u64 key[kSplitIpt][KW];
+#pragma unroll
+  for (int u = 0; u < kSplitIpt; ++u) {  // all loads in flight before the table is ready
+    const uint32_t t = T.t0 + u * kSplitTileThreads + threadIdx.x;
+    if (t < T.t1) {
+      load_key<KW>(K1, D.n, t, key[u]);
+    } else {
+#pragma unroll
+      for (int d = 0; d < KW; ++d) key[u][d] = 0;
+    }
+  }
+  __syncthreads();
+  uint32_t w[kSplitIpt];
+  int pos[kSplitIpt];
+#pragma unroll
+  for (int u = 0; u < kSplitIpt; ++u) {
+    w[u] = (uint32_t)(get_seg<KW>(key[u], cp, 64) >> 32);
+    pos[u] = 0;
+  }
+  // number of splitter windows <= w (padding compares greater unless w is maximal)
+#pragma unroll
+  for (int st = kSplitWinSlots / 2; st > 0; st >>= 1) {
+#pragma unroll
+    for (int u = 0; u < kSplitIpt; ++u)
+      if (SPW[pos[u] + st - 1] <= w[u]) pos[u] += st;
+  }
+#pragma unroll
+  for (int u = 0; u < kSplitIpt; ++u) {
+    const uint32_t t = T.t0 + u * kSplitTileThreads + threadIdx.x;
+    if (t >= T.t1) continue;
+    int q = pos[u] < nsp ? pos[u] : nsp;
+    // splitters with the key's own window count only if they are <= the key
+    while (q > 0 && SPW[q - 1] == w[u] && key_lt<KW>(key[u], SPF, D.max_sub, q - 1)) --q;
+    SID[t] = (uint16_t)q;
+    atomicAdd(&hist[q], 1u);
   }
   __syncthreads();
   uint32_t* g = C.sub_count + (int64_t)T.b * D.max_sub;
@@ -1267,36 +1325,61 @@ static __global__ void __launch_bounds__(1024) k_split_bases(Dims D, Ctl C) {
   }
 }
 
+// Scatter of a tile into the sub-buckets.  Every load of the tile (sub-bucket
+// ids, ik, and the keys when they are narrow) is issued before the first
+// barrier and the items wait in registers, so a CTA exposes one DRAM latency
+// instead of one per loop iteration.
 template <int KW>
 __global__ void __launch_bounds__(kSplitTileThreads)
 k_split_scatter(Dims D, Ctl C) {
   extern __shared__ u64 sm[];
-  u64* SP = sm;
-  uint32_t* hist = reinterpret_cast<uint32_t*>(SP + (int64_t)KW * D.max_sub);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sm);
   uint32_t* gbase = hist + D.max_sub;
-  uint32_t* code = gbase + D.max_sub;  // per item: sub << 16 | rank
+  constexpr bool STAGE = KW <= 2;  // wider keys are re-read when written
   SplitTile T;
-  if (!split_tile_setup<KW>(D, C, SP, hist, T)) return;
+  if (!split_tile_setup(D, C, hist, T)) return;
   const u64* K1 = C.k1 + T.base;
   const uint32_t* I1 = C.i1 + T.base;
-  for (uint32_t t = T.t0 + threadIdx.x; t < T.t1; t += kSplitTileThreads) {
-    u64 key[KW];
-    load_key<KW>(K1, D.n, t, key);
-    const int q = bucket_of<KW>(key, SP, D.max_sub, T.nsub - 1);
-    code[t - T.t0] = ((uint32_t)q << 16) | atomicAdd(&hist[q], 1u);
+  const uint16_t* SID = C.sid + T.base;
+  uint32_t sub[kSplitIpt], ik[kSplitIpt];
+  u64 key[kSplitIpt][STAGE ? KW : 1];
+#pragma unroll
+  for (int u = 0; u < kSplitIpt; ++u) {
+    const uint32_t t = T.t0 + u * kSplitTileThreads + threadIdx.x;
+    sub[u] = 0xFFFFFFFFu;
+    if (t < T.t1) {
+      sub[u] = SID[t];
+      ik[u] = I1[t];
+      if (STAGE) {
+#pragma unroll
+        for (int d = 0; d < (STAGE ? KW : 1); ++d) key[u][d] = K1[d * D.n + t];
+      }
+    }
   }
+  __syncthreads();  // histogram cleared
+  uint32_t rank[kSplitIpt];
+#pragma unroll
+  for (int u = 0; u < kSplitIpt; ++u)
+    if (sub[u] != 0xFFFFFFFFu) rank[u] = atomicAdd(&hist[sub[u]], 1u);
   __syncthreads();
   uint32_t* g = C.sub_count + (int64_t)T.b * D.max_sub;
   for (int q = threadIdx.x; q < T.nsub; q += kSplitTileThreads)
     if (hist[q]) gbase[q] = atomicAdd(&g[q], hist[q]);
   __syncthreads();
-  for (uint32_t t = T.t0 + threadIdx.x; t < T.t1; t += kSplitTileThreads) {
-    const uint32_t cd = code[t - T.t0];
-    const uint32_t pos = gbase[cd >> 16] + (cd & 0xFFFFu);
-    u64 key[KW];
-    load_key<KW>(K1, D.n, t, key);
-    store_key<KW>(C.k2, D.n, pos, key);
-    C.i2[pos] = I1[t];
+#pragma unroll
+  for (int u = 0; u < kSplitIpt; ++u) {
+    if (sub[u] == 0xFFFFFFFFu) continue;
+    const uint32_t pos = gbase[sub[u]] + rank[u];
+    if (STAGE) {
+#pragma unroll
+      for (int d = 0; d < (STAGE ? KW : 1); ++d) C.k2[d * D.n + pos] = key[u][d];
+    } else {
+      const uint32_t t = T.t0 + u * kSplitTileThreads + threadIdx.x;
+      u64 kk[KW];
+      load_key<KW>(K1, D.n, t, kk);
+      store_key<KW>(C.k2, D.n, pos, kk);
+    }
+    C.i2[pos] = ik[u];
   }
 }
 
@@ -1305,8 +1388,9 @@ static int launch_split(const pl_merge_plan& P, const Dims& D, const Ctl& C, cud
   const int s2cap = (int)P.reserved[1];
   const size_t psm = sample_smem_bytes(s2cap, KW);
   if (set_smem(k_split_prep<KW>, psm)) return PL_ERR_CUDA;
-  const size_t tsm = (size_t)8 * KW * D.max_sub + 8 * (size_t)D.max_sub + 4 * (size_t)kSplitTile + 64;
-  if (set_smem(k_split_count<KW>, tsm)) return PL_ERR_CUDA;
+  const size_t csm = 4 * (size_t)kSplitWinSlots + 4 * (size_t)D.max_sub + 64;  // windows | histogram
+  const size_t tsm = 8 * (size_t)D.max_sub + 64;  // histogram | bases
+  if (set_smem(k_split_count<KW>, csm)) return PL_ERR_CUDA;
   if (set_smem(k_split_scatter<KW>, tsm)) return PL_ERR_CUDA;
   const unsigned max_tiles = (unsigned)(ceil_div(D.n, (int64_t)kSplitTile) + D.nb1);
   {
@@ -1316,7 +1400,7 @@ static int launch_split(const pl_merge_plan& P, const Dims& D, const Ctl& C, cud
   }
   {
     StageTimer t_(st, "k_split_count");
-    k_split_count<KW><<<max_tiles, kSplitTileThreads, tsm, st>>>(D, C);
+    k_split_count<KW><<<max_tiles, kSplitTileThreads, csm, st>>>(D, C);
     PLB_CHECK_LAUNCH("k_split_count");
   }
   {
@@ -1344,7 +1428,7 @@ static inline int64_t align256(int64_t v) { return (v + 255) & ~(int64_t)255; }
 struct WsLayout {
   int64_t split, bcount, bbase, bcursor, leaf_off, n_leaves, leaf_ctr, tile_off, n_tiles,
       sub_count, leaf_desc, split2, kept, kprefix, scan, k1, i1, k2, i2, sums, rmap, opk, opb, l1tab,
-      perm, total;
+      perm, split2w, bcp, bid, sid, total;
 };
 
 // Bound on the number of leaves: a bucket of s items gets at most
@@ -1353,6 +1437,17 @@ static inline int64_t plan_max_leaves(const pl_merge_plan& P) {
   const int64_t by_sub = (int64_t)P.n_buckets * P.max_sub;
   const int64_t by_size = P.n_items / std::max(1, P.leaf_target) + P.n_buckets + 1;
   return std::min(by_sub, by_size);
+}
+
+// Slots of the per-item level-1 bucket ids: whole generator CTAs (kTileA x
+// kTileB tiles of the outer product, kGenThreads * kGenTB terms of a sort).
+static inline int64_t gen_slots(const pl_merge_plan& P) {
+  const int64_t per = (int64_t)kGenThreads * kGenTB;
+  if (P.mode == 0 && P.ma > 0) {
+    const int64_t cols = ceil_div(P.n_items, P.ma);  // B columns generated here
+    return ceil_div(P.ma, (int64_t)kTileA) * ceil_div(cols, (int64_t)kTileB) * per;
+  }
+  return ceil_div(P.n_items, per) * per;
 }
 
 static WsLayout ws_layout(const pl_merge_plan& P) {
@@ -1387,6 +1482,10 @@ static WsLayout ws_layout(const pl_merge_plan& P) {
   w.opb = o; o = align256(o + (P.ma + P.mb));
   w.l1tab = o; o = align256(o + 2 * ((1 << kTabBits) + 1));
   w.perm = o; o = align256(o + 4 * (P.ma + P.mb));
+  w.split2w = o; o = align256(o + 8 * sub_slots);
+  w.bcp = o; o = align256(o + 4 * nb1);
+  w.bid = o; o = align256(o + 2 * gen_slots(P));
+  w.sid = o; o = align256(o + 2 * n);
   w.total = o;
   (void)ctl_end;
   return w;
@@ -1625,6 +1724,10 @@ static Ctl to_ctl(const pl_merge_plan& P, void* ws) {
   C.opb = (uint8_t*)(b + w.opb);
   C.l1tab = (uint16_t*)(b + w.l1tab);
   C.perm = (int32_t*)(b + w.perm);
+  C.split2w = (u64*)(b + w.split2w);
+  C.bcp = (int32_t*)(b + w.bcp);
+  C.bid = (uint16_t*)(b + w.bid);
+  C.sid = (uint16_t*)(b + w.sid);
   C.k1 = (u64*)(b + w.k1);
   C.i1 = (uint32_t*)(b + w.i1);
   C.k2 = (u64*)(b + w.k2);
@@ -1704,10 +1807,11 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S0, void* ws, const 
     PLB_CHECK_LAUNCH("k_buckets");
   }
   // 4. scatter
-  if (set_smem(k_scatter<W, KW, MODE>, gsm)) return PL_ERR_CUDA;
+  const size_t ssm = gen_smem_bytes(W, KW, D.nb1, false);
+  if (set_smem(k_scatter<W, KW, MODE>, ssm)) return PL_ERR_CUDA;
   {
     StageTimer t_(st, "k_scatter");
-    k_scatter<W, KW, MODE><<<ggrid, kGenThreads, gsm, st>>>(L, D, S, C);
+    k_scatter<W, KW, MODE><<<ggrid, kGenThreads, ssm, st>>>(L, D, S, C);
     PLB_CHECK_LAUNCH("k_scatter");
   }
   // 5. level-2 split of oversized buckets
@@ -1836,10 +1940,11 @@ static int run_partition(const pl_merge_plan& P, const SrcA& S, int64_t j0, int6
       k_buckets<<<1, 1024, 0, st>>>(D, C, (int64_t*)(C.n_leaves + 2));
       PLB_CHECK_LAUNCH("k_buckets");
     }
-    if (set_smem(k_scatter<W, KW, 0>, gsm)) return PL_ERR_CUDA;
+    const size_t ssm = gen_smem_bytes(W, KW, D.nb1, false);
+    if (set_smem(k_scatter<W, KW, 0>, ssm)) return PL_ERR_CUDA;
     {
       StageTimer t_(st, "k_scatter");
-      k_scatter<W, KW, 0><<<ggrid, kGenThreads, gsm, st>>>(L, D, S, C);
+      k_scatter<W, KW, 0><<<ggrid, kGenThreads, ssm, st>>>(L, D, S, C);
       PLB_CHECK_LAUNCH("k_scatter");
     }
     StageTimer t_(st, "k_pack");

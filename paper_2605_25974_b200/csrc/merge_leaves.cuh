@@ -237,7 +237,8 @@ constexpr int kRankDups = 2;      // *perm holds the order, some keys are equal
 // warp-total buffers (four barriers per pass).
 template <int KW, int CAP>
 __device__ __noinline__ int radix_rank_leaf(const u64* K, const uint32_t* I, int n,
-                                            uint8_t* scratch, uint16_t** perm) {
+                                            uint8_t* scratch, uint16_t** perm,
+                                            const u64 (&diff)[KW]) {
   static_assert(CAP % kLeafThreads2 == 0, "leaf capacity must be a multiple of the CTA size");
   constexpr int SEG = CAP / kLeafWarps2;             // max positions owned by one warp
   constexpr int SLOTS = SEG >= 32 ? SEG / 32 : 1;
@@ -255,14 +256,11 @@ __device__ __noinline__ int radix_rank_leaf(const u64* K, const uint32_t* I, int
   __shared__ uint32_t s_scan[2][kLeafWarps2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  // 1. highest bit at which any key differs from item 0
+  // 1. highest bit at which any key differs from item 0 (diff: this thread's
+  //    OR of key ^ key 0 over the items it staged)
   u64 acc[KW];
 #pragma unroll
-  for (int d = 0; d < KW; ++d) acc[d] = 0;
-  for (int t = tid; t < n; t += kLeafThreads2) {
-#pragma unroll
-    for (int d = 0; d < KW; ++d) acc[d] |= K[d * CAP + t] ^ K[d * CAP];
-  }
+  for (int d = 0; d < KW; ++d) acc[d] = diff[d];
 #pragma unroll
   for (int d = 0; d < KW; ++d) {
 #pragma unroll
@@ -434,9 +432,10 @@ __device__ __forceinline__ void apply_leaf_perm(u64* K, uint32_t* I, int n, cons
 
 // Sorts the leaf in place; false = not sorted (the caller runs the bitonic network).
 template <int KW, int CAP>
-__device__ __forceinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint8_t* scratch) {
+__device__ __forceinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint8_t* scratch,
+                                                const u64 (&diff)[KW]) {
   uint16_t* sp = nullptr;
-  if (radix_rank_leaf<KW, CAP>(K, I, n, scratch, &sp) == kRankFallback) return false;
+  if (radix_rank_leaf<KW, CAP>(K, I, n, scratch, &sp, diff) == kRankFallback) return false;
   apply_leaf_perm<KW, CAP>(K, I, n, sp);
   return true;
 }
@@ -487,13 +486,21 @@ __device__ __noinline__ uint32_t leaf_sort_global(const Dims& D, const SrcA& S, 
   // 1. sorted tiles
   for (int t0 = 0; t0 < n; t0 += cap) {
     const int m = min(cap, n - t0);
+    u64 diff[KW];
+#pragma unroll
+    for (int d = 0; d < KW; ++d) diff[d] = 0;
     for (int t = tid; t < m; t += kLeafThreads2) {
 #pragma unroll
-      for (int d = 0; d < KW; ++d) SK[d * cap + t] = K[d * stride + t0 + t];
+      for (int d = 0; d < KW; ++d) {
+        const u64 v = K[d * stride + t0 + t];
+        SK[d * cap + t] = v;
+        diff[d] |= v ^ K[d * stride + t0];
+      }
       SI[t] = I[t0 + t];
     }
     __syncthreads();
-    if (m > 1 && !radix_sort_leaf<KW, cap>(SK, SI, m, scratch)) bitonic_sort_local<KW, cap>(SK, SI, m);
+    if (m > 1 && !radix_sort_leaf<KW, cap>(SK, SI, m, scratch, diff))
+      bitonic_sort_local<KW, cap>(SK, SI, m);
     for (int t = tid; t < m; t += kLeafThreads2) {
 #pragma unroll
       for (int d = 0; d < KW; ++d) K[d * stride + t0 + t] = SK[d * cap + t];
@@ -628,16 +635,29 @@ k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
     return;
   }
   double2* SUM = reinterpret_cast<double2*>(scratch);  // reuses the radix scratch
-  for (int t = tid; t < n; t += kLeafThreads2) {
+  u64 diff[KW];  // OR of key ^ key 0 over this thread's items (the radix window start)
+  {
+    u64 k0[KW];
 #pragma unroll
-    for (int d = 0; d < KW; ++d) K[d * cap + t] = GK[d * D.n + t];
-    I[t] = GI[t];
+    for (int d = 0; d < KW; ++d) {
+      k0[d] = __ldg(GK + d * D.n);
+      diff[d] = 0;
+    }
+    for (int t = tid; t < n; t += kLeafThreads2) {
+#pragma unroll
+      for (int d = 0; d < KW; ++d) {
+        const u64 v = GK[d * D.n + t];
+        K[d * cap + t] = v;
+        diff[d] |= v ^ k0[d];
+      }
+      I[t] = GI[t];
+    }
   }
   __syncthreads();
   LEAF_T(1);
   if (n > 1) {
     uint16_t* sp = nullptr;
-    const int rank = radix_rank_leaf<KW, cap>(K, I, n, scratch, &sp);
+    const int rank = radix_rank_leaf<KW, cap>(K, I, n, scratch, &sp, diff);
     if (rank == kRankDistinct) {
       // Every key of the leaf differs: each item is its own run, so nothing is
       // moved in shared memory -- rank t's key and coefficient go straight to
@@ -646,24 +666,26 @@ k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
       double2 cf[PERF];
       int src[PERF];
       bool drop = false;
+      // the keys go out first (asynchronous stores; the general path below
+      // rewrites the leaf's slots if a term is dropped), then the coefficients
 #pragma unroll
       for (int r = 0; r < PERF; ++r) {
         const int t = r * kLeafThreads2 + tid;
         src[r] = t < n ? (int)sp[t] : -1;
-        if (t < n) cf[r] = Source<W, KW, MODE>::coef(S, D.ma, I[src[r]]);
+        if (src[r] < 0) continue;
+#pragma unroll
+        for (int d = 0; d < KW; ++d) DK[d * D.n + t] = K[d * cap + src[r]];
       }
+#pragma unroll
+      for (int r = 0; r < PERF; ++r)
+        if (src[r] >= 0) cf[r] = Source<W, KW, MODE>::coef(S, D.ma, I[src[r]]);
 #pragma unroll
       for (int r = 0; r < PERF; ++r)
         if (src[r] >= 0 && !keep_sum(cf[r], eps)) drop = true;
       if (!__syncthreads_or(drop)) {
 #pragma unroll
-        for (int r = 0; r < PERF; ++r) {
-          const int t = r * kLeafThreads2 + tid;
-          if (src[r] < 0) continue;
-#pragma unroll
-          for (int d = 0; d < KW; ++d) DK[d * D.n + t] = K[d * cap + src[r]];
-          DS[t] = cf[r];
-        }
+        for (int r = 0; r < PERF; ++r)
+          if (src[r] >= 0) DS[r * kLeafThreads2 + tid] = cf[r];
         if (tid == 0) C.kept[leaf] = (uint32_t)n;
         return;
       }
