@@ -417,7 +417,10 @@ def main():
             return pl.sum_multiply(Ah, Bh)
 
         r = e2e_step()                                   # warm-up (pinned pools)
-        d2h = sum_bytes(r)
+        # bytes actually copied: planes that are zero in every operand are
+        # cleared on the host instead of crossing PCIe (sums._download)
+        d2h = int(pl.sums.LAST_D2H_BYTES)
+        result_bytes = sum_bytes(r)
         del r
         barrier()
         torch.cuda.synchronize()
@@ -434,6 +437,7 @@ def main():
             el = float(t.item())
         e2e = {"value": n_items * ne / el, "unit": UNIT,
                "h2d_bytes_per_step": sum_bytes(A) + sum_bytes(B), "d2h_bytes_per_step": d2h,
+               "host_result_bytes_per_step": result_bytes,
                "ms_per_step": 1e3 * el / ne}
 
     # ---- CPU baseline and secondary workloads (rank 0 at N=1 only)

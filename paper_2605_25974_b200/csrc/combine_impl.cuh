@@ -59,7 +59,7 @@ constexpr int kSample1Oversample = 16;  // level-1 samples per bucket
 constexpr int kLeavesPerBucket = 32;
 constexpr int kTabBits = 13;  // level-1 prefix table: splitters per top-13-bit key prefix
 constexpr int kMaxBuckets = 2048;
-constexpr int kSplitTile = 1024;     // items per level-2 classification tile
+constexpr int kSplitTile = 2048;     // items per level-2 classification tile
 constexpr int kSplitTileThreads = 256;
 
 // ---------------------------------------------------------------- layout
@@ -87,7 +87,10 @@ struct Ctl {  // control arrays inside the workspace
   int32_t* bcp;          // nb1: bits shared by every key of the bucket (window offset)
   uint16_t* bid;         // level-1 bucket of every generated item (k_count -> k_scatter)
   uint16_t* sid;         // [n] level-2 sub-bucket of every item (k_split_count -> k_split_scatter)
-  uint32_t* sub_count;   // [nb1][max_sub] level-2 counts, then cursors
+  uint32_t* sub_count;   // [nb1][max_sub] first output position of every sub-bucket
+  uint4* tile_desc;      // per level-2 tile: (bucket, first item, items, sub-buckets)
+  uint16_t* thist;       // [tiles][max_sub] items of the tile per sub-bucket
+  uint32_t* toff;        // [tiles][max_sub] offset of the tile's run inside the sub-bucket
   uint32_t* tile_off;    // nb1 + 1: first split tile of each bucket
   uint32_t* n_tiles;     // 1
   uint32_t* kept;         // max_leaves: merged terms per leaf
@@ -1139,6 +1142,14 @@ k_split_prep(Dims D, Ctl C, int s2cap) {
     return;
   }
   const int nsub = leaves_for(size, D);
+  {  // descriptors of the bucket's level-2 tiles
+    const uint32_t nt = (size + kSplitTile - 1) / kSplitTile, t_first = C.tile_off[b];
+    for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) {
+      const uint32_t first = i * kSplitTile;
+      C.tile_desc[t_first + i] = make_uint4((uint32_t)b, base + first,
+                                            min((uint32_t)kSplitTile, size - first), (uint32_t)nsub);
+    }
+  }
   int ns = nsub * kSampleOversample;
   if (ns > s2cap) ns = s2cap;
   if ((uint32_t)ns > size) ns = (int)size;
@@ -1188,62 +1199,37 @@ k_split_prep(Dims D, Ctl C, int s2cap) {
   }
 }
 
-// tile t -> its bucket (last b with tile_off[b] <= t; tile_off non-decreasing,
-// tile_off[0] == 0).  Warp-cooperative 32-ary search: every round the lanes
-// probe 32 evenly spaced entries of the current range at once, so nb1 <= 1024
-// takes two rounds of one load each instead of ten dependent loads.
-__device__ __forceinline__ int tile_bucket_warp(const Ctl& C, int nb1, uint32_t t) {
-  const int lane = threadIdx.x & 31;
-  int lo = 0, len = nb1;  // answer in [lo, lo + len)
-  while (len > 1) {
-    const int step = (len + 31) / 32;
-    const int idx = lo + lane * step;
-    const bool le = idx < lo + len && C.tile_off[idx] <= t;
-    const unsigned m = __ballot_sync(0xffffffffu, le);  // lane 0 always set
-    const int hi_lane = 31 - __clz((int)m);
-    const int nlo = lo + hi_lane * step;
-    len = min(step, lo + len - nlo);
-    lo = nlo;
-  }
-  return lo;
-}
-
+// One level-2 tile: kSplitTile consecutive items of a split bucket
+// (descriptors written by k_split_prep).
 struct SplitTile {
   int b, nsub;
-  uint32_t base, size, t0, t1;  // bucket base/size; item range [t0, t1) inside the bucket
+  uint32_t first, count;  // first item (absolute) and number of items
 };
 
-// Locates the CTA's tile (bucket, item range) and clears the tile histogram;
-// false if the grid has no such tile.
-__device__ __forceinline__ bool split_tile_setup(const Dims& D, const Ctl& C, uint32_t* hist,
-                                                 SplitTile& T) {
-  __shared__ int s_b;
+__device__ __forceinline__ bool split_tile_load(const Ctl& C, SplitTile& T) {
   const uint32_t t = blockIdx.x;
+  const uint4 d = C.tile_desc[t];  // in bounds (grid = the tile bound); valid below n_tiles
   if (t >= *C.n_tiles) return false;
-  if (threadIdx.x < 32) {
-    const int b = tile_bucket_warp(C, D.nb1, t);
-    if (threadIdx.x == 0) s_b = b;
-  }
-  __syncthreads();
-  T.b = s_b;
-  T.base = C.bbase[T.b];
-  T.size = C.bcount[T.b];
-  T.nsub = leaves_for(T.size, D);
-  T.t0 = (t - C.tile_off[T.b]) * kSplitTile;
-  T.t1 = min(T.size, T.t0 + kSplitTile);
-  for (int q = threadIdx.x; q < T.nsub; q += blockDim.x) hist[q] = 0;
+  T.b = (int)d.x;
+  T.first = d.y;
+  T.count = d.z;
+  T.nsub = (int)d.w;
   return true;
 }
 
 constexpr int kSplitIpt = kSplitTile / kSplitTileThreads;  // items per thread
+constexpr int kSplitIlp = 4;                                // searches interleaved per thread
 constexpr int kSplitWinSlots = 1024;                        // padded window table (>= max_sub)
+static_assert(kSplitIpt % kSplitIlp == 0, "tile items per thread");
 
 // Level-2 classification searches 32-bit windows: the key bits after the
 // prefix every key of the bucket shares (C.bcp) -- one shared-memory word and
 // one compare per step of a fixed ten-step search over a table padded with
-// the maximal window, a thread's items interleaved.  Splitters whose window
-// equals the key's (rare) are compared in full from global memory.  Every
-// item's sub-bucket goes to C.sid, so k_split_scatter does not search again.
+// the maximal window, four items interleaved.  Splitters whose window equals
+// the key's (rare) are compared in full from global memory.  Every item's
+// sub-bucket goes to C.sid (k_split_scatter does not search again) and the
+// tile's histogram to C.thist: k_split_bases turns the histograms of a bucket
+// into the position of every (tile, sub-bucket) run, so no global atomics.
 template <int KW>
 __global__ void __launch_bounds__(kSplitTileThreads)
 k_split_count(Dims D, Ctl C) {
@@ -1251,84 +1237,110 @@ k_split_count(Dims D, Ctl C) {
   uint32_t* SPW = reinterpret_cast<uint32_t*>(sm);  // [kSplitWinSlots] splitter windows
   uint32_t* hist = SPW + kSplitWinSlots;
   SplitTile T;
-  if (!split_tile_setup(D, C, hist, T)) return;
+  if (!split_tile_load(C, T)) return;
   const int nsp = T.nsub - 1;
   {
     const u64* G = C.split2w + (int64_t)T.b * D.max_sub;
-    for (int q = threadIdx.x; q < kSplitWinSlots; q += blockDim.x)
+    for (int q = threadIdx.x; q < kSplitWinSlots; q += blockDim.x) {
       SPW[q] = q < nsp ? (uint32_t)(G[q] >> 32) : 0xFFFFFFFFu;
+      if (q < D.max_sub) hist[q] = 0;
+    }
   }
   const int cp = C.bcp[T.b];
-  const u64* K1 = C.k1 + T.base;
+  const u64* K1 = C.k1 + T.first;
   const u64* SPF = C.split2 + (int64_t)T.b * KW * D.max_sub;
-  uint16_t* SID = C.sid + T.base;
-  u64 key[kSplitIpt][KW];
+  uint16_t* SID = C.sid + T.first;
+  __syncthreads();
+#pragma unroll 1
+  for (int h = 0; h < kSplitIpt; h += kSplitIlp) {
+    u64 key[kSplitIlp][KW];
+    uint32_t w[kSplitIlp];
+    int pos[kSplitIlp];
 #pragma unroll
-  for (int u = 0; u < kSplitIpt; ++u) {  // all loads in flight before the table is ready
-    const uint32_t t = T.t0 + u * kSplitTileThreads + threadIdx.x;
-    if (t < T.t1) {
-      load_key<KW>(K1, D.n, t, key[u]);
-    } else {
+    for (int u = 0; u < kSplitIlp; ++u) {
+      const uint32_t t = (h + u) * kSplitTileThreads + threadIdx.x;
 #pragma unroll
-      for (int d = 0; d < KW; ++d) key[u][d] = 0;
+      for (int d = 0; d < KW; ++d) key[u][d] = t < T.count ? K1[d * D.n + t] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kSplitIlp; ++u) {
+      w[u] = (uint32_t)(get_seg<KW>(key[u], cp, 64) >> 32);
+      pos[u] = 0;
+    }
+    // number of splitter windows <= w (padding compares greater unless w is maximal)
+#pragma unroll
+    for (int st = kSplitWinSlots / 2; st > 0; st >>= 1) {
+#pragma unroll
+      for (int u = 0; u < kSplitIlp; ++u)
+        if (SPW[pos[u] + st - 1] <= w[u]) pos[u] += st;
+    }
+#pragma unroll
+    for (int u = 0; u < kSplitIlp; ++u) {
+      const uint32_t t = (h + u) * kSplitTileThreads + threadIdx.x;
+      if (t >= T.count) continue;
+      int q = pos[u] < nsp ? pos[u] : nsp;
+      // splitters with the key's own window count only if they are <= the key
+      while (q > 0 && SPW[q - 1] == w[u] && key_lt<KW>(key[u], SPF, D.max_sub, q - 1)) --q;
+      SID[t] = (uint16_t)q;
+      atomicAdd(&hist[q], 1u);
     }
   }
   __syncthreads();
-  uint32_t w[kSplitIpt];
-  int pos[kSplitIpt];
-#pragma unroll
-  for (int u = 0; u < kSplitIpt; ++u) {
-    w[u] = (uint32_t)(get_seg<KW>(key[u], cp, 64) >> 32);
-    pos[u] = 0;
-  }
-  // number of splitter windows <= w (padding compares greater unless w is maximal)
-#pragma unroll
-  for (int st = kSplitWinSlots / 2; st > 0; st >>= 1) {
-#pragma unroll
-    for (int u = 0; u < kSplitIpt; ++u)
-      if (SPW[pos[u] + st - 1] <= w[u]) pos[u] += st;
-  }
-#pragma unroll
-  for (int u = 0; u < kSplitIpt; ++u) {
-    const uint32_t t = T.t0 + u * kSplitTileThreads + threadIdx.x;
-    if (t >= T.t1) continue;
-    int q = pos[u] < nsp ? pos[u] : nsp;
-    // splitters with the key's own window count only if they are <= the key
-    while (q > 0 && SPW[q - 1] == w[u] && key_lt<KW>(key[u], SPF, D.max_sub, q - 1)) --q;
-    SID[t] = (uint16_t)q;
-    atomicAdd(&hist[q], 1u);
-  }
-  __syncthreads();
-  uint32_t* g = C.sub_count + (int64_t)T.b * D.max_sub;
-  for (int q = threadIdx.x; q < T.nsub; q += kSplitTileThreads)
-    if (hist[q]) atomicAdd(&g[q], hist[q]);
+  uint16_t* th = C.thist + (int64_t)blockIdx.x * D.max_sub;
+  for (int q = threadIdx.x; q < T.nsub; q += kSplitTileThreads) th[q] = (uint16_t)hist[q];
 }
 
+// CTA per split bucket, thread per sub-bucket: walks the bucket's tiles in
+// order, turning each tile's count into the offset of its run inside the
+// sub-bucket (C.toff), then scans the sub-bucket totals into the leaf
+// descriptors and the sub-buckets' first positions (C.sub_count).
 static __global__ void __launch_bounds__(1024) k_split_bases(Dims D, Ctl C) {
   const int b = blockIdx.x;
   const uint32_t size = C.bcount[b];
   if ((int)size <= D.leaf_cap) return;
   const uint32_t base = C.bbase[b], lo = C.leaf_off[b];
   const int nsub = leaves_for(size, D);
+  const uint32_t t0 = C.tile_off[b], nt = (size + kSplitTile - 1) / kSplitTile;
   uint32_t* g = C.sub_count + (int64_t)b * D.max_sub;
   uint32_t carry = 0;
   for (int q0 = 0; q0 < nsub; q0 += blockDim.x) {
     const int q = q0 + threadIdx.x;
-    const uint32_t h = q < nsub ? g[q] : 0u;
+    uint32_t h = 0;
+    if (q < nsub) {
+      const uint16_t* th = C.thist + (int64_t)t0 * D.max_sub + q;
+      uint32_t* to = C.toff + (int64_t)t0 * D.max_sub + q;
+      uint32_t i = 0;
+      for (; i + 4 <= nt; i += 4) {  // four tiles' counts in flight
+        uint32_t c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) c[u] = th[(int64_t)(i + u) * D.max_sub];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          to[(int64_t)(i + u) * D.max_sub] = h;
+          h += c[u];
+        }
+      }
+      for (; i < nt; ++i) {
+        const uint32_t c = th[(int64_t)i * D.max_sub];
+        to[(int64_t)i * D.max_sub] = h;
+        h += c;
+      }
+    }
     uint32_t tot;
     const uint32_t ex = block_excl_scan(h, &tot) + carry;
     if (q < nsub) {
       C.leaf_desc[lo + q] = make_uint4(2u, base + ex, h, 0u);
-      g[q] = base + ex;  // cursor
+      g[q] = base + ex;
     }
     carry += tot;
   }
 }
 
 // Scatter of a tile into the sub-buckets.  Every load of the tile (sub-bucket
-// ids, ik, and the keys when they are narrow) is issued before the first
-// barrier and the items wait in registers, so a CTA exposes one DRAM latency
-// instead of one per loop iteration.
+// ids, ik, the keys when they are narrow, and the positions of the tile's
+// runs) is issued up front and the items wait in registers, so a CTA exposes
+// one memory latency after its descriptor; ranks inside a run come from
+// shared-memory atomics.
 template <int KW>
 __global__ void __launch_bounds__(kSplitTileThreads)
 k_split_scatter(Dims D, Ctl C) {
@@ -1337,17 +1349,17 @@ k_split_scatter(Dims D, Ctl C) {
   uint32_t* gbase = hist + D.max_sub;
   constexpr bool STAGE = KW <= 2;  // wider keys are re-read when written
   SplitTile T;
-  if (!split_tile_setup(D, C, hist, T)) return;
-  const u64* K1 = C.k1 + T.base;
-  const uint32_t* I1 = C.i1 + T.base;
-  const uint16_t* SID = C.sid + T.base;
+  if (!split_tile_load(C, T)) return;
+  const u64* K1 = C.k1 + T.first;
+  const uint32_t* I1 = C.i1 + T.first;
+  const uint16_t* SID = C.sid + T.first;
   uint32_t sub[kSplitIpt], ik[kSplitIpt];
   u64 key[kSplitIpt][STAGE ? KW : 1];
 #pragma unroll
   for (int u = 0; u < kSplitIpt; ++u) {
-    const uint32_t t = T.t0 + u * kSplitTileThreads + threadIdx.x;
+    const uint32_t t = u * kSplitTileThreads + threadIdx.x;
     sub[u] = 0xFFFFFFFFu;
-    if (t < T.t1) {
+    if (t < T.count) {
       sub[u] = SID[t];
       ik[u] = I1[t];
       if (STAGE) {
@@ -1356,16 +1368,19 @@ k_split_scatter(Dims D, Ctl C) {
       }
     }
   }
-  __syncthreads();  // histogram cleared
+  {
+    const uint32_t* g = C.sub_count + (int64_t)T.b * D.max_sub;
+    const uint32_t* to = C.toff + (int64_t)blockIdx.x * D.max_sub;
+    for (int q = threadIdx.x; q < T.nsub; q += kSplitTileThreads) {
+      hist[q] = 0;
+      gbase[q] = g[q] + to[q];
+    }
+  }
+  __syncthreads();
   uint32_t rank[kSplitIpt];
 #pragma unroll
   for (int u = 0; u < kSplitIpt; ++u)
     if (sub[u] != 0xFFFFFFFFu) rank[u] = atomicAdd(&hist[sub[u]], 1u);
-  __syncthreads();
-  uint32_t* g = C.sub_count + (int64_t)T.b * D.max_sub;
-  for (int q = threadIdx.x; q < T.nsub; q += kSplitTileThreads)
-    if (hist[q]) gbase[q] = atomicAdd(&g[q], hist[q]);
-  __syncthreads();
 #pragma unroll
   for (int u = 0; u < kSplitIpt; ++u) {
     if (sub[u] == 0xFFFFFFFFu) continue;
@@ -1374,7 +1389,7 @@ k_split_scatter(Dims D, Ctl C) {
 #pragma unroll
       for (int d = 0; d < (STAGE ? KW : 1); ++d) C.k2[d * D.n + pos] = key[u][d];
     } else {
-      const uint32_t t = T.t0 + u * kSplitTileThreads + threadIdx.x;
+      const uint32_t t = u * kSplitTileThreads + threadIdx.x;
       u64 kk[KW];
       load_key<KW>(K1, D.n, t, kk);
       store_key<KW>(C.k2, D.n, pos, kk);
@@ -1392,7 +1407,7 @@ static int launch_split(const pl_merge_plan& P, const Dims& D, const Ctl& C, cud
   const size_t tsm = 8 * (size_t)D.max_sub + 64;  // histogram | bases
   if (set_smem(k_split_count<KW>, csm)) return PL_ERR_CUDA;
   if (set_smem(k_split_scatter<KW>, tsm)) return PL_ERR_CUDA;
-  const unsigned max_tiles = (unsigned)(ceil_div(D.n, (int64_t)kSplitTile) + D.nb1);
+  const unsigned max_tiles = (unsigned)(ceil_div(D.n, (int64_t)kSplitTile) + D.nb1);  // = plan_max_tiles of the layout's plan
   {
     StageTimer t_(st, "k_split_prep");
     k_split_prep<KW><<<D.nb1, kSplitThreads, psm, st>>>(D, C, s2cap);
@@ -1428,7 +1443,7 @@ static inline int64_t align256(int64_t v) { return (v + 255) & ~(int64_t)255; }
 struct WsLayout {
   int64_t split, bcount, bbase, bcursor, leaf_off, n_leaves, leaf_ctr, tile_off, n_tiles,
       sub_count, leaf_desc, split2, kept, kprefix, scan, k1, i1, k2, i2, sums, rmap, opk, opb, l1tab,
-      perm, split2w, bcp, bid, sid, total;
+      perm, split2w, bcp, bid, sid, tile_desc, thist, toff, total;
 };
 
 // Bound on the number of leaves: a bucket of s items gets at most
@@ -1437,6 +1452,11 @@ static inline int64_t plan_max_leaves(const pl_merge_plan& P) {
   const int64_t by_sub = (int64_t)P.n_buckets * P.max_sub;
   const int64_t by_size = P.n_items / std::max(1, P.leaf_target) + P.n_buckets + 1;
   return std::min(by_sub, by_size);
+}
+
+// Bound on the level-2 tiles: every split bucket has ceil(size / kSplitTile).
+static inline int64_t plan_max_tiles(const pl_merge_plan& P) {
+  return ceil_div(P.n_items, (int64_t)kSplitTile) + P.n_buckets;
 }
 
 // Slots of the per-item level-1 bucket ids: whole generator CTAs (kTileA x
@@ -1486,6 +1506,10 @@ static WsLayout ws_layout(const pl_merge_plan& P) {
   w.bcp = o; o = align256(o + 4 * nb1);
   w.bid = o; o = align256(o + 2 * gen_slots(P));
   w.sid = o; o = align256(o + 2 * n);
+  const int64_t max_tiles = plan_max_tiles(P);
+  w.tile_desc = o; o = align256(o + 16 * max_tiles);
+  w.thist = o; o = align256(o + 2 * max_tiles * P.max_sub);
+  w.toff = o; o = align256(o + 4 * max_tiles * P.max_sub);
   w.total = o;
   (void)ctl_end;
   return w;
@@ -1728,6 +1752,9 @@ static Ctl to_ctl(const pl_merge_plan& P, void* ws) {
   C.bcp = (int32_t*)(b + w.bcp);
   C.bid = (uint16_t*)(b + w.bid);
   C.sid = (uint16_t*)(b + w.sid);
+  C.tile_desc = (uint4*)(b + w.tile_desc);
+  C.thist = (uint16_t*)(b + w.thist);
+  C.toff = (uint32_t*)(b + w.toff);
   C.k1 = (u64*)(b + w.k1);
   C.i1 = (uint32_t*)(b + w.i1);
   C.k2 = (u64*)(b + w.k2);

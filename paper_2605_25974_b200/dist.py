@@ -28,7 +28,8 @@ import torch.distributed as dist
 
 from . import _native
 from ._device import cuda_device, ptr, stream_ptr
-from .sums import PauliSumSoA, _alloc_planes, _download, _fitted, _new_sum, _remember
+from .sums import (PauliSumSoA, _alloc_planes, _download, _fitted, _new_sum, _remember,
+                   _zero_planes)
 
 
 def block_range(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -140,7 +141,7 @@ def sharded_outer_multiply(a: PauliSumSoA, b: PauliSumSoA, *, group=None, eps: f
         out = merge_received(A, B, plan, recv, cm, b0, b1, eps, dev, a.n)
     else:  # fewer buckets than ranks: this rank owns no key range (still joined the exchange)
         out = PauliSumSoA.empty(a.n, device=dev)
-    return _download(out) if back else out
+    return _download(out, *_zero_planes(plan), True) if back else out
 
 
 def emulate_sharded(a: PauliSumSoA, b: PauliSumSoA, world: int, *, eps: float = 0.0):

@@ -470,17 +470,61 @@ def _remember(plan) -> None:
                   "leaf_cap", "leaf_target", "max_sub", "workspace_bytes")}
 
 
-def _download(s: PauliSumSoA) -> PauliSumSoA:
-    """Device result -> host sum through pinned staging buffers (torch's caching
-    host allocator recycles them), one async copy per array, then one sync."""
-    def pinned(t):
-        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-        h.copy_(t, non_blocking=True)
-        return h
+LAST_D2H_BYTES = 0  # instrumentation: bytes the most recent _download copied from the device
 
-    x, z, k, c = (pinned(t) for t in (s.x, s.z, s.flags, s.coeffs))
+
+def _zero_planes(plan) -> tuple[frozenset, frozenset]:
+    """Plane words (x, z) that are zero in every term a merge can produce: the
+    plan keeps no bit of a canonical-key word whose OR over the operands is
+    zero (``seg_len`` 0; key words are z[0..W) then x[0..W), sums.py:104-106),
+    and products/merges only XOR and copy operand words."""
+    W = int(plan.W)
+    zz = frozenset(w for w in range(W) if int(plan.seg_len[w]) == 0)
+    zx = frozenset(w for w in range(W) if int(plan.seg_len[W + w]) == 0)
+    return zx, zz
+
+
+def _download(s: PauliSumSoA, zero_x=frozenset(), zero_z=frozenset(),
+              zero_flags: bool = False) -> PauliSumSoA:
+    """Device result -> host sum through pinned staging buffers (torch's caching
+    host allocator recycles them): asynchronous copies, then one sync.
+
+    Planes the caller proves zero (``_zero_planes``; the phase bytes of a
+    combined sum) are not read over PCIe: they are cleared on the host while
+    the DMA of the other arrays runs (n=500 sums on 48 qubits: 14 of the 16
+    planes)."""
+    global LAST_D2H_BYTES
+    copied = 0
+
+    def pinned_like(t):
+        return torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+
+    def fetch(h, t):
+        nonlocal copied
+        h.copy_(t, non_blocking=True)
+        copied += t.numel() * t.element_size()
+
+    W = s.x.shape[0]
+    hx, hz, hk, hc = (pinned_like(t) for t in (s.x, s.z, s.flags, s.coeffs))
+    fetch(hc, s.coeffs)
+    for h, t, zero in ((hx, s.x, zero_x), (hz, s.z, zero_z)):
+        if not zero:
+            fetch(h, t)
+        else:
+            for w in range(W):
+                if w not in zero:
+                    fetch(h[w], t[w])
+    if not zero_flags:
+        fetch(hk, s.flags)
+    # host-side clears overlap the copies in flight
+    for h, zero in ((hx, zero_x), (hz, zero_z)):
+        for w in sorted(zero):
+            h[w].zero_()
+    if zero_flags:
+        hk.zero_()
     torch.cuda.current_stream(s.device).synchronize()
-    return _new_sum(s.n, x, z, k, c)
+    LAST_D2H_BYTES = copied
+    return _new_sum(s.n, hx, hz, hk, hc)
 
 
 def _new_sum(n, x, z, k, c) -> PauliSumSoA:
@@ -537,6 +581,7 @@ def outer_multiply(a: PauliSumSoA, b: PauliSumSoA, *, eps: float = 0.0, combine:
     W, ma, mb = A.W, A.M, B.M
     n_items = ma * mb
     st = stream_ptr(dev)
+    zero = ()
     with torch.cuda.device(dev):
         if n_items == 0:
             out = PauliSumSoA.empty(a.n, device=dev)
@@ -566,7 +611,8 @@ def outer_multiply(a: PauliSumSoA, b: PauliSumSoA, *, eps: float = 0.0, combine:
                 _native.call("pl_outer_multiply_combine", C.byref(plan), *args,
                              ptr(x), ptr(z), ptr(k), ptr(c), x.stride(0), ptr(cnt), st)
                 out = _fitted(a.n, x, z, k, c, int(cnt.item()))
-    return _download(out) if back else out
+            zero = (*_zero_planes(plan), True)  # combined terms carry phase 0
+    return _download(out, *zero) if back else out
 
 
 def sort_combine(s: PauliSumSoA, *, eps: float = 0.0) -> PauliSumSoA:
@@ -577,6 +623,7 @@ def sort_combine(s: PauliSumSoA, *, eps: float = 0.0) -> PauliSumSoA:
     S = s.to(dev).planes()
     W, m = S.W, S.M
     st = stream_ptr(dev)
+    zero = ()
     with torch.cuda.device(dev):
         if m == 0:
             out = PauliSumSoA.empty(s.n, device=dev)
@@ -596,7 +643,8 @@ def sort_combine(s: PauliSumSoA, *, eps: float = 0.0) -> PauliSumSoA:
                 _native.call("pl_sort_combine", C.byref(plan), *args,
                              ptr(x), ptr(z), ptr(k), ptr(c), x.stride(0), ptr(cnt), st)
                 out = _fitted(s.n, x, z, k, c, int(cnt.item()))
-    return _download(out) if back else out
+            zero = (*_zero_planes(plan), True)
+    return _download(out, *zero) if back else out
 
 
 # ------------------------------------------------------- module functions

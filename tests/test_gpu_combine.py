@@ -179,6 +179,31 @@ def test_determinism_and_host_path(cuda):
     assert isinstance(aos, pl.PauliSum) and len(aos) == len(r1)
 
 
+def test_host_path_zero_planes_on_dirty_buffers(cuda):
+    """Host results: planes proved zero by the plan are cleared on the host,
+    not copied.  Recycled pinned buffers hold stale data (a dense result
+    first), so a missed clear would show; sort_and_combine shares the path."""
+    from paper_2605_25974_b200 import sums as S
+    ax, az, af, ac = rng.random_columns(500, 300, 7)
+    dense = pl.PauliSumSoA.from_columns(500, ax, az, af, ac)          # every plane nonzero
+    sparse_a, sparse_b = rng.config_columns(2, scale=0.3)              # qubits 0..23 only
+    A, B = soa(500, sparse_a, None), soa(500, sparse_b, None)
+    for _ in range(2):
+        d = pl.sort_and_combine(dense)                                 # dirties the pinned pool
+        assert S.LAST_D2H_BYTES == d.payload_nbytes - len(d)           # only the phase bytes skipped
+        del d
+        h = pl.sum_multiply(A, B)
+        assert h.device.type == "cpu"
+        m = len(h)
+        assert S.LAST_D2H_BYTES == m * (2 * 8 + 16)                    # x0, z0 and the coefficients
+        ref = pl.sum_multiply(A.cuda(), B.cuda()).cpu()
+        assert h == ref
+        assert not h.x[1:].any() and not h.z[1:].any() and not h.flags.any()
+        hs = pl.sort_and_combine(pl.sum_multiply(A, B, combine=False))
+        assert hs == ref
+        del h, hs
+
+
 def test_raw_count_exact(cuda):
     """|output before combine| = |a|*|b| exactly."""
     a, b = rng.config_columns(2, scale=0.05)
