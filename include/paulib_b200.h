@@ -267,6 +267,21 @@ int pl_rotation_split(int W, int64_t M, const uint64_t* x, const uint64_t* z, co
                       int64_t ldo, int64_t* out_count, void* stream);
 
 /* ------------------------------------------------------------------------
+ * §8(f) f4 — packed AoS records <-> SoA planes.  Replaces the host transposes
+ * of PauliSum.to_soa (sums.py:417-426) and PauliSumSoA.to_aos (sums.py:469-477)
+ * for sums that live on (or are headed to) the device.  `records` is a DEVICE
+ * array of M packed records of 16W + 17 bytes, the reference's aos_dtype
+ * (sums.py:48-57): x[W] u64 | z[W] u64 | flags u8 | coeff (re, im) f64, no
+ * padding; it must be 16-byte aligned.  Planes have leading dimension ld >= M.
+ * Exact bijection in both directions.  pl_soa_to_aos accepts k == NULL (flags 0).
+ */
+int pl_aos_to_soa(int W, int64_t M, const void* records,
+                  uint64_t* x, uint64_t* z, uint8_t* k, double* c, int64_t ld, void* stream);
+int pl_soa_to_aos(int W, int64_t M,
+                  const uint64_t* x, const uint64_t* z, const uint8_t* k, const double* c,
+                  int64_t ld, void* records, void* stream);
+
+/* ------------------------------------------------------------------------
  * Stage timing (instrumentation for bench.py).  While enabled, multi-kernel
  * entry points record a CUDA event pair around every kernel they launch, on
  * the launching stream.  pl_stage_times() waits for the recorded events and

@@ -45,7 +45,10 @@ def u64_to_i64_tensor(a) -> torch.Tensor:
             return a.view(torch.int64)
         raise TypeError(f"bit planes must be 64-bit integer tensors, got {a.dtype}")
     arr = np.ascontiguousarray(np.asarray(a, dtype=np.uint64))
-    if not arr.flags.writeable:  # e.g. PauliString's read-only planes: torch needs writable
+    # torch needs writable memory (PauliString's planes are read-only) and
+    # strides in whole elements (a one-record field view of packed AoS records
+    # is "contiguous" with the record's odd stride)
+    if not arr.flags.writeable or any(st % arr.itemsize for st in arr.strides):
         arr = arr.copy()
     return torch.from_numpy(arr.view(np.int64))
 

@@ -70,6 +70,8 @@ SIGNATURES = {
     "pl_bitmatrix_workspace_bytes": (_L, [_I, _L]),
     "pl_group_workspace_bytes": (_L, [_I, _L]),
     "pl_group_greedy": (_I, [_I, _L, _P, _P, _L, _P, _P, _P, _P, _S, _P]),
+    "pl_aos_to_soa": (_I, [_I, _L, _P, _P, _P, _P, _P, _L, _P]),
+    "pl_soa_to_aos": (_I, [_I, _L, _P, _P, _P, _P, _L, _P, _P]),
     "pl_merge_emit": (_I, [C.POINTER(MergePlan), _P, _S, _P, _P, _P, _P, _L, _L, _P, _P]),
     "pl_dist_item_bytes": (_I, [C.POINTER(MergePlan)]),
     "pl_dist_workspace_bytes": (_L, [C.POINTER(MergePlan), _L, C.c_int32]),

@@ -36,7 +36,7 @@ namespace plb {
 
 constexpr int kGB = 1024;              // batch size (terms)
 constexpr int kGAW = kGB / 32;         // anti-row words per term
-constexpr int kGK = 4;                 // first-k fitting groups kept per term
+constexpr int kGK = 16;                // first-k fitting groups listed per term
 constexpr int kSlotChunks = kGB / 64 + 2;
 constexpr int kHash = 2048;            // resolver hash slots (power of 2)
 
@@ -93,14 +93,16 @@ __device__ bool deep_fit(const GCtx& G, int g, const uint16_t* lst, uint32_t cnt
   return true;
 }
 
+constexpr int kFitThreads = 256;  // batch terms per k_group_fit CTA (blockIdx.y = term block)
+
 template <int W>
-__global__ void __launch_bounds__(kGB, 1) k_group_fit(GCtx G, int64_t b0, int bn) {
+__global__ void __launch_bounds__(kFitThreads) k_group_fit(GCtx G, int64_t b0, int bn) {
   constexpr int E = 128 * W;
   constexpr int GPC = 8;  // groups per shared-memory pass (8 KB x W)
   extern __shared__ u64 S[];  // [GPC][E]
   if (*G.overflow) return;
   const uint32_t G0 = *G.gcur;
-  const int t = threadIdx.x;
+  const int t = blockIdx.y * kFitThreads + threadIdx.x;
   const bool valid = t < bn;
   uint32_t off = 0, cnt = 0;
   if (valid) {
@@ -182,6 +184,33 @@ __global__ void __launch_bounds__(1024) k_group_firstk(GCtx G, int bn) {
 }
 
 // ------------------------------------------------------------ resolver
+// One warp replays the batch in term order, 32 terms (one per lane) at a time.
+//
+// Per group touched in the batch ("slot") the warp keeps BLOCKED[slot]: the OR
+// of the intra-batch anti rows of the batch terms placed in it, so "does a
+// batch member of the group anti-commute with term i" is ONE bit test (round
+// 1 ANDed the term's anti row with the group's member mask: a 32-word
+// reduction per candidate, every candidate a dependent chain on one warp,
+// ~1000 cycles per term, 57% of config 3).
+//
+// Sub-block j = batch terms 32j..32j+31.  Its anti rows and candidate lists
+// (the first kGK fitting old groups of every term, k_group_firstk) are staged
+// in shared memory.  Rounds until every lane is settled:
+//   1. every unsettled lane advances its own cursor over its candidate list
+//      to the first group not blocked by the COMMITTED members (bit test);
+//   2. a lane's pick is void if an earlier unsettled lane picked the same
+//      group and anti-commutes with it (match.any + word j of the anti row),
+//      or if it has no old group left ("hard");
+//   3. the lanes before the first void one are committed together (slots,
+//      member ranks, BLOCKED |= their anti rows).  A void pick becomes blocked
+//      by that commit, so its cursor moves on in the next round; a hard lane
+//      is settled alone: the rest of its fit0 row from global memory (when it
+//      fits more than kGK old groups), then the groups opened in this batch,
+//      32 per step (one bit test per lane), else a new group.
+// Blocked bits only ever get set, so cursors never move back; the outcome is
+// exactly the sequential first-fit.
+constexpr int kMaskLd = kGAW + 1;  // padded rows: lanes reading one word of 32 rows hit 32 banks
+
 struct ResolveSmem {
   int32_t hkey[kHash];
   int32_t hval[kHash];
@@ -189,7 +218,9 @@ struct ResolveSmem {
   int32_t slot_old[kGB];
   int32_t slot_cnt[kGB];
   int32_t newg[kGB];
-  uint32_t mask[kGB][kGAW];
+  uint32_t aw[32 * kMaskLd];        // anti rows of the current sub-block (whole rows)
+  int32_t cl[32 * (kGK + 1)];       // candidate lists of the current sub-block (padded rows)
+  uint32_t blocked[kGB * kMaskLd];  // per slot: batch terms anti-commuting with a placed member
 };
 
 __device__ __forceinline__ int hfind(const ResolveSmem& R, int g) {
@@ -209,108 +240,217 @@ __device__ __forceinline__ void hinsert(ResolveSmem& R, int g, int s) {
   R.hval[h] = s;
 }
 
+struct ResolveState {
+  uint32_t G0, gcur;
+  int nslots, nnew;
+  bool ovf;
+};
+
+// New slot for group g (warp-uniform): old = 0 for a group opened in this
+// batch, -1 for a pre-existing one (its size is loaded after the replay).
+__device__ __forceinline__ int new_slot(ResolveSmem& R, ResolveState& T, int g, int old) {
+  const int lane = threadIdx.x;
+  const int s = T.nslots++;
+  if (lane == 0) {
+    R.slot_group[s] = g;
+    R.slot_old[s] = old;
+    R.slot_cnt[s] = 0;
+    hinsert(R, g, s);
+  }
+  R.blocked[s * kMaskLd + lane] = 0u;
+  __syncwarp();
+  return s;
+}
+
+// Settles batch term i alone (warp-uniform): the old groups after its listed
+// candidates (last = the last listed one, -1 if the list was complete), the
+// groups opened in this batch, else a new group.
+__device__ __forceinline__ void resolve_hard(const GCtx& G, ResolveSmem& R, ResolveState& T,
+                                             int64_t b0, int i, int64_t nwords, int last) {
+  const int lane = threadIdx.x;
+  const int l = i & 31, j = i >> 5;
+  int chosen = -1, s = -1;
+  if (last >= 0) {  // more than kGK fitting old groups: the row after group `last`, 32 words per step
+    const uint32_t* row = G.fit0 + (int64_t)i * G.gw_stride;
+    const int64_t w0 = (last + 1) / 32;
+    for (int64_t base = w0; base < nwords && chosen < 0; base += 32) {
+      const int64_t w = base + lane;
+      uint32_t v = w < nwords ? row[w] : 0u;
+      if (w == w0) v &= ~((1u << ((last + 1) & 31)) - 1u);
+      unsigned nz = __ballot_sync(0xffffffffu, v != 0u);
+      while (nz && chosen < 0) {
+        const int src = __ffs(nz) - 1;
+        nz &= nz - 1;
+        uint32_t bits = __shfl_sync(0xffffffffu, v, src);
+        while (bits && chosen < 0) {
+          const int c = (int)((base + src) * 32) + __ffs(bits) - 1;
+          bits &= bits - 1;
+          const int sl = hfind(R, c);
+          if (sl < 0 || !(R.blocked[sl * kMaskLd + j] >> l & 1u)) {
+            chosen = c;
+            s = sl;
+          }
+        }
+      }
+    }
+    if (chosen >= 0 && s < 0) s = new_slot(R, T, chosen, -1);
+  }
+  for (int k0 = 0; k0 < T.nnew && chosen < 0; k0 += 32) {  // opened in this batch, creation order
+    const int kk = k0 + lane;
+    int sl = -1;
+    bool ok = false;
+    if (kk < T.nnew) {
+      sl = R.newg[kk];
+      ok = !(R.blocked[sl * kMaskLd + j] >> l & 1u);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    if (m) {
+      s = __shfl_sync(0xffffffffu, sl, __ffs(m) - 1);
+      chosen = R.slot_group[s];
+    }
+  }
+  if (chosen < 0) {
+    if ((int64_t)T.gcur >= G.gcap) {
+      T.ovf = true;
+      return;
+    }
+    chosen = (int)T.gcur++;
+    s = new_slot(R, T, chosen, 0);
+    if (lane == 0) R.newg[T.nnew] = s;
+    ++T.nnew;
+  }
+  R.blocked[s * kMaskLd + lane] |= R.aw[l * kMaskLd + lane];
+  if (lane == 0) {
+    G.group_of[b0 + i] = chosen;
+    G.member[i] = (uint32_t)R.slot_cnt[s];  // rank among this batch's members
+    G.tslot[i] = s;
+    R.slot_cnt[s] += 1;
+  }
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int bn) {
   extern __shared__ uint8_t smraw[];
   ResolveSmem& R = *reinterpret_cast<ResolveSmem*>(smraw);
   if (*G.overflow) return;
   const int lane = threadIdx.x;
+  const unsigned lt_mask = (1u << lane) - 1u;
   for (int i = lane; i < kHash; i += 32) R.hkey[i] = -1;
   __syncwarp();
-  const uint32_t G0 = *G.gcur;
-  uint32_t gcur = G0;
-  int nslots = 0, nnew = 0;
-  bool ovf = false;
-  // software prefetch of the next term's anti row and candidates
-  uint32_t aw_n = bn > 0 ? G.anti[lane] : 0u;
-  int nf_n = bn > 0 ? G.nfit[0] : 0;
-  int32_t fk_n = (bn > 0 && lane < kGK) ? G.fitk[lane] : -1;
-  for (int i = 0; i < bn && !ovf; ++i) {
-    // anti-commutation with earlier batch terms only (u < i)
-    uint32_t aw = aw_n;
-    const int nf = nf_n;
-    const int32_t fk = fk_n;
-    if (i + 1 < bn) {
-      aw_n = G.anti[(int64_t)(i + 1) * kGAW + lane];
-      nf_n = G.nfit[i + 1];
-      fk_n = lane < kGK ? G.fitk[(i + 1) * kGK + lane] : -1;
+  ResolveState T;
+  T.G0 = *G.gcur;
+  T.gcur = T.G0;
+  T.nslots = 0;
+  T.nnew = 0;
+  T.ovf = false;
+  const int64_t nwords = ((int64_t)T.G0 + 31) / 32;
+  // the next sub-block's anti rows and candidate lists wait in registers
+  // (coalesced: 32 rows of 32 words; 32 lists of kGK ids = kGK words per lane)
+  uint32_t nx[kGAW];
+  int32_t ncl[kGK];
+  int nnf = lane < bn ? G.nfit[lane] : 0;
+#pragma unroll
+  for (int r = 0; r < kGAW; ++r) nx[r] = r < bn ? G.anti[(int64_t)r * kGAW + lane] : 0u;
+#pragma unroll
+  for (int r = 0; r < kGK; ++r) ncl[r] = G.fitk[r * 32 + lane];  // (in bounds: kGB lists)
+  for (int i0 = 0, j = 0; i0 < bn && !T.ovf; i0 += 32, ++j) {
+    const int cnt = bn - i0 < 32 ? bn - i0 : 32;
+#pragma unroll
+    for (int r = 0; r < kGAW; ++r) R.aw[r * kMaskLd + lane] = nx[r];
+#pragma unroll
+    for (int r = 0; r < kGK; ++r) {
+      const int e = r * 32 + lane;  // list e / kGK, entry e % kGK
+      R.cl[(e / kGK) * (kGK + 1) + (e % kGK)] = ncl[r];
     }
-    const int wi = i >> 5;
-    aw = lane < wi ? aw : (lane == wi ? (aw & ((1u << (i & 31)) - 1u)) : 0u);
-    int chosen = -1, cslot = -2;  // cslot: slot of `chosen` (-1 none yet, -2 unknown)
+    const int nf = nnf;                       // fitting old groups (kGK + 1 = more than listed)
     const int ncand = nf < kGK ? nf : kGK;
-    for (int k = 0; k < ncand && chosen < 0; ++k) {
-      const int c = __shfl_sync(0xffffffffu, fk, k);
-      const int s = hfind(R, c);
-      if (s < 0 || !__any_sync(0xffffffffu, (aw & R.mask[s][lane]) != 0u)) {
-        chosen = c;
-        cslot = s;
+    if (i0 + 32 < bn) {
+#pragma unroll
+      for (int r = 0; r < kGAW; ++r) {
+        const int64_t t = i0 + 32 + r;
+        nx[r] = t < bn ? G.anti[t * kGAW + lane] : 0u;
       }
-    }
-    if (chosen < 0 && nf > kGK) {  // rare: all first-k candidates blocked
-      const int64_t nwords = ((int64_t)G0 + 31) / 32;
-      const uint32_t* row = G.fit0 + (int64_t)i * G.gw_stride;
-      const int last = __shfl_sync(0xffffffffu, fk, kGK - 1);
-      for (int64_t w = (last + 1) / 32; w < nwords && chosen < 0; ++w) {
-        uint32_t bits = row[w];
-        if (w == (last + 1) / 32) bits &= ~((1u << ((last + 1) & 31)) - 1u);
-        while (bits && chosen < 0) {
-          const int c = (int)(w * 32) + __ffs(bits) - 1;
-          bits &= bits - 1;
-          const int s = hfind(R, c);
-          if (s < 0 || !__any_sync(0xffffffffu, (aw & R.mask[s][lane]) != 0u)) chosen = c;
-        }
-      }
-    }
-    if (chosen < 0) {  // groups opened earlier in this batch, creation order
-      for (int k = 0; k < nnew && chosen < 0; ++k) {
-        const int s = R.newg[k];
-        if (!__any_sync(0xffffffffu, (aw & R.mask[s][lane]) != 0u)) chosen = R.slot_group[s];
-      }
-    }
-    int s;
-    if (chosen < 0) {
-      if ((int64_t)gcur >= G.gcap) {
-        ovf = true;
-        break;
-      }
-      chosen = (int)gcur++;
-      s = nslots++;
-      if (lane == 0) {
-        R.slot_group[s] = chosen;
-        R.slot_old[s] = 0;
-        R.slot_cnt[s] = 0;
-        R.newg[nnew] = s;
-        hinsert(R, chosen, s);
-      }
-      R.mask[s][lane] = 0u;
-      ++nnew;
-    } else {
-      s = cslot != -2 ? cslot : hfind(R, chosen);
-      if (s < 0) {
-        s = nslots++;
-        if (lane == 0) {
-          R.slot_group[s] = chosen;
-          R.slot_old[s] = -1;  // pre-existing group: size loaded after the loop
-          R.slot_cnt[s] = 0;
-          hinsert(R, chosen, s);
-        }
-        R.mask[s][lane] = 0u;
-      }
+#pragma unroll
+      for (int r = 0; r < kGK; ++r) ncl[r] = G.fitk[(i0 + 32) * kGK + r * 32 + lane];
+      nnf = i0 + 32 + lane < bn ? G.nfit[i0 + 32 + lane] : 0;
     }
     __syncwarp();
-    if (lane == wi) R.mask[s][lane] |= 1u << (i & 31);
-    if (lane == 0) {
-      G.group_of[b0 + i] = chosen;
-      G.member[i] = (uint32_t)R.slot_cnt[s];  // rank among this batch's members
-      G.tslot[i] = s;
-      R.slot_cnt[s] += 1;
+    const uint32_t arow_j = R.aw[lane * kMaskLd + j] & lt_mask;  // anti with earlier lanes
+    unsigned todo = cnt == 32 ? 0xffffffffu : ((1u << cnt) - 1u);  // unsettled lanes
+    int ck = 0;                                                    // cursor into the candidate list
+    while (todo && !T.ovf) {
+      const bool mine = todo >> lane & 1u;
+      // 1. first fitting old group not blocked by the committed members
+      int cand = -1, cslot = -1;
+      if (mine) {
+        for (; ck < ncand; ++ck) {
+          const int c = R.cl[lane * (kGK + 1) + ck];
+          const int sl = hfind(R, c);
+          if (sl < 0 || !(R.blocked[sl * kMaskLd + j] >> lane & 1u)) {
+            cand = c;
+            cslot = sl;
+            break;
+          }
+        }
+      }
+      // 2. void picks: an earlier unsettled lane took the same group and anti-commutes
+      const unsigned have = __ballot_sync(0xffffffffu, mine && cand >= 0);
+      bool bad = mine && cand < 0;
+      if (mine && cand >= 0) {
+        const unsigned peers = __match_any_sync(have, cand);
+        bad = (arow_j & peers) != 0u;
+      }
+      const unsigned badm = __ballot_sync(0xffffffffu, bad);
+      const int first_bad = badm ? __ffs(badm) - 1 : 32;
+      const unsigned okm = todo & (first_bad >= 32 ? 0xffffffffu : ((1u << first_bad) - 1u));
+      // 3. commit the lanes before the first void one
+      if (okm) {
+        const bool done = okm >> lane & 1u;
+        unsigned need = __ballot_sync(0xffffffffu, done && cslot < 0);
+        while (need) {  // slots for groups first touched in this batch
+          const int c0 = __shfl_sync(0xffffffffu, cand, __ffs(need) - 1);
+          const int s = new_slot(R, T, c0, -1);
+          if (done && cslot < 0 && cand == c0) cslot = s;
+          need = __ballot_sync(0xffffffffu, done && cslot < 0);
+        }
+        if (done) {
+          const unsigned peers = __match_any_sync(okm, cslot);
+          const int before = __popc(peers & lt_mask);
+          const int base = R.slot_cnt[cslot];
+          __syncwarp(okm);
+          if (before == 0) R.slot_cnt[cslot] = base + __popc(peers);
+          const int i = i0 + lane;
+          G.group_of[b0 + i] = cand;
+          G.member[i] = (uint32_t)(base + before);  // rank among this batch's members
+          G.tslot[i] = cslot;
+        }
+        __syncwarp();
+        for (unsigned m = okm; m; m &= m - 1) {  // BLOCKED[slot] |= the member's anti row
+          const int l = __ffs(m) - 1;
+          const int s = __shfl_sync(0xffffffffu, cslot, l);
+          R.blocked[s * kMaskLd + lane] |= R.aw[l * kMaskLd + lane];
+        }
+        __syncwarp();
+        todo &= ~okm;
+      }
+      if (first_bad < 32) {
+        const bool hard = __shfl_sync(0xffffffffu, (int)(cand < 0), first_bad) != 0;
+        if (hard) {
+          const int nfb = __shfl_sync(0xffffffffu, nf, first_bad);
+          const int last = nfb > kGK ? R.cl[first_bad * (kGK + 1) + kGK - 1] : -1;
+          resolve_hard(G, R, T, b0, i0 + first_bad, nwords, last);
+          todo &= ~(1u << first_bad);
+        }
+        // a void pick is blocked by the commit above: its cursor moves on next round
+      }
     }
-    __syncwarp();
   }
-  if (ovf) {
+  if (T.ovf) {
     if (lane == 0) *G.overflow = 1;
     return;
   }
+  const int nslots = T.nslots;
+  const uint32_t gcur = T.gcur;
   // grow every touched group: allocate chunks, link, record chunk tables
   for (int s = lane; s < nslots; s += 32) {
     const int g = R.slot_group[s];
@@ -557,7 +697,9 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
     }
     if (b0 > 0) {
       StageTimer t_(st, "k_group_fit");
-      k_group_fit<W><<<fit_grid, kGB, fit_smem, st>>>(G, b0, bn);
+      // term blocks x group words: few groups (config 3: 23 words) still fill the SMs
+      k_group_fit<W><<<dim3((unsigned)fit_grid, kGB / kFitThreads), kFitThreads, fit_smem, st>>>(
+          G, b0, bn);
     }
     {
       StageTimer t_(st, "k_group_firstk");

@@ -249,7 +249,10 @@ class PauliSumSoA:
         return f"PauliSumSoA(n={self.n}, terms={len(self)}, device={self.device})"
 
     def to_aos(self) -> "PauliSum":
-        """Inverse of PauliSum.to_soa (sums.py:469-477)."""
+        """Inverse of PauliSum.to_soa (sums.py:469-477).  A device sum is
+        transposed into packed records on the GPU and comes back in one copy."""
+        if self.device.type == "cuda":
+            return PauliSum(self.n, _download_aos(self))
         return PauliSum.from_columns(self.n, *self.columns())
 
     def _check_same_n(self, other) -> None:
@@ -400,7 +403,11 @@ class PauliSum:
         return self.term(i).string.canonical_key()
 
     def to_soa(self, device=None) -> PauliSumSoA:
-        """Transpose into SoA planes (sums.py:417-426); ``device`` optional."""
+        """Transpose into SoA planes (sums.py:417-426).  With a CUDA ``device``
+        the packed records are uploaded as they are and transposed on the GPU
+        (``pl_aos_to_soa``); without one the result stays on the host."""
+        if device is not None and torch.device(device).type == "cuda":
+            return _upload_aos(self.n, self._data, torch.device(device))
         d = self._data
         return PauliSumSoA(self.n, np.ascontiguousarray(d["x"].T), np.ascontiguousarray(d["z"].T),
                            d["flags"].copy(), d["coeff"].copy(), device=device, validate=False)
@@ -421,15 +428,16 @@ class PauliSum:
 
     def multiply(self, other, *, threads: int = 1, eps: float = 0.0, combine: bool = True):
         self._check_same_n(other)
-        b = other.to_soa() if isinstance(other, PauliSum) else other
-        return self.to_soa().multiply(b, eps=eps, combine=combine).to_aos()
+        dev = cuda_device(other.device if isinstance(other, PauliSumSoA) else None)
+        b = other.to_soa(dev) if isinstance(other, PauliSum) else other
+        return self.to_soa(dev).multiply(b, eps=eps, combine=combine).to_aos()
 
     __mul__ = multiply
 
     def sort_and_combine(self, eps: float = 0.0):
         if eps < 0:
             raise ValueError("eps must be >= 0")
-        return self.to_soa().sort_and_combine(eps).to_aos()
+        return self.to_soa(cuda_device()).sort_and_combine(eps).to_aos()
 
     def apply_clifford(self, gate: str, qubits) -> None:
         """In place on the packed records (sums.py:309-316): the records are
@@ -442,7 +450,7 @@ class PauliSum:
 
     def apply_rotation(self, rot, *, eps: float = 0.0, combine: bool = True):
         """sums.py:318-325."""
-        return self.to_soa().apply_rotation(rot, eps=eps, combine=combine).to_aos()
+        return self.to_soa(cuda_device()).apply_rotation(rot, eps=eps, combine=combine).to_aos()
 
     def truncate(self, eps: float):
         if eps < 0:
@@ -525,6 +533,43 @@ def _download(s: PauliSumSoA, zero_x=frozenset(), zero_z=frozenset(),
     torch.cuda.current_stream(s.device).synchronize()
     LAST_D2H_BYTES = copied
     return _new_sum(s.n, hx, hz, hk, hc)
+
+
+def _upload_aos(n: int, data: np.ndarray, dev: torch.device) -> PauliSumSoA:
+    """Packed host records -> device SoA planes: one H2D copy of the records,
+    transposed by ``pl_aos_to_soa`` (sums.py:417-426 on the GPU)."""
+    W = tier_for(n) // 64
+    m = int(data.shape[0])
+    if m == 0:
+        return PauliSumSoA.empty(n, device=dev)
+    raw = np.ascontiguousarray(data).view(np.uint8).reshape(-1)
+    if not raw.flags.writeable:
+        raw = raw.copy()
+    with torch.cuda.device(dev):
+        d_raw = torch.from_numpy(raw).to(dev)
+        x, z, k, c = _alloc_planes(W, m, dev)
+        _native.call("pl_aos_to_soa", W, m, ptr(d_raw), ptr(x), ptr(z), ptr(k), ptr(c),
+                     x.stride(0), stream_ptr(dev))
+    return _new_sum(n, x, z, k, c)
+
+
+def _download_aos(s: PauliSumSoA) -> np.ndarray:
+    """Device SoA planes -> packed host records (``pl_soa_to_aos`` + one D2H
+    copy into pinned memory); the array views that pinned buffer."""
+    W, m = s.words, len(s)
+    dt = aos_dtype(W)
+    if m == 0:
+        return np.empty(0, dtype=dt)
+    dev = s.device
+    S = s.planes()
+    with torch.cuda.device(dev):
+        rec = torch.empty(m * dt.itemsize, dtype=torch.uint8, device=dev)
+        _native.call("pl_soa_to_aos", W, m, ptr(S.x), ptr(S.z), ptr(S.k), ptr(S.c), S.ld,
+                     ptr(rec), stream_ptr(dev))
+        h = torch.empty(m * dt.itemsize, dtype=torch.uint8, pin_memory=True)
+        h.copy_(rec, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+    return h.numpy().view(dt)
 
 
 def _new_sum(n, x, z, k, c) -> PauliSumSoA:

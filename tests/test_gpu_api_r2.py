@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import paper_2605_25974_b200 as pl
+from paper_2605_25974_b200 import rng
 from conftest import golden
 
 pytestmark = pytest.mark.gpu
@@ -66,3 +67,34 @@ def test_negative_eps_keeps_exact_zeros(cuda):
     assert np.abs(c - g["rc"]).max() <= 1e-12 * np.abs(g["rc"]).sum()
     with pytest.raises(ValueError):
         pl.sort_and_combine(H, eps=-1.0)  # the public sort_and_combine still rejects it
+
+
+@pytest.mark.parametrize("n", [40, 100, 200, 500, 1000])
+@pytest.mark.parametrize("m", [0, 1, 15, 128, 129, 1000])
+def test_aos_soa_device_transpose(cuda, n, m):
+    """f4: packed records <-> device planes (sums.py:417-426, :469-477) is the
+    exact bijection the host transposes compute, at every tier and across
+    tile boundaries (tiles of 128 records)."""
+    x, z, f, c = rng.random_columns(n, max(m, 1), 11)
+    x, z, f, c = x[:m], z[:m], f[:m], c[:m]
+    f = (np.arange(m) % 4).astype(np.uint8)
+    aos = pl.PauliSum.from_columns(n, x, z, f, c)
+    dev_soa = aos.to_soa(device=cuda)
+    assert dev_soa.device.type == "cuda" and len(dev_soa) == m
+    host_soa = aos.to_soa()
+    assert dev_soa.cpu() == host_soa
+    back = dev_soa.to_aos()
+    assert isinstance(back, pl.PauliSum) and back == aos
+
+
+def test_aos_multiply_runs_on_device_records(cuda):
+    """PauliSum.multiply uploads the records, multiplies on the GPU and returns
+    records transposed on the GPU: same terms as the SoA path."""
+    a, b = rng.config_columns(2, scale=0.2)
+    A, B = pl.PauliSum.from_columns(500, *a), pl.PauliSum.from_columns(500, *b)
+    got = A.multiply(B)
+    ref = pl.sum_multiply(pl.PauliSumSoA.from_columns(500, *a, device=cuda),
+                          pl.PauliSumSoA.from_columns(500, *b, device=cuda))
+    assert got == ref.cpu().to_aos()
+    assert A.sort_and_combine() == pl.sort_and_combine(
+        pl.PauliSumSoA.from_columns(500, *a, device=cuda)).cpu().to_aos()
