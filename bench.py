@@ -366,9 +366,12 @@ def main():
     ent_b = 8 * kw + 16                       # merged (key, sum) entry
     term_b = 16 * 8 + 1 + 16                  # SoA output term at W=8
     algo = {
-        "k_scatter": (local_items * item_b, f"{item_b} B item written"),
-        "k_split_count": (local_items * 8 * kw, f"{8 * kw} B item key read"),
-        "k_split_scatter": (2 * local_items * item_b, f"{item_b} B item read + written"),
+        "k_count": (local_items * 2, "2 B bucket id written (items are generated, not read)"),
+        "k_scatter": (local_items * (item_b + 2), f"2 B bucket id read + {item_b} B item written"),
+        "k_split_count": (local_items * (8 * kw + 2),
+                          f"{8 * kw} B item key read + 2 B sub-bucket id written"),
+        "k_split_scatter": (local_items * (2 * item_b + 2),
+                            f"{item_b} B item + 2 B sub-bucket id read, {item_b} B item written"),
         "k_leaf_sort": (local_items * item_b + local_out * ent_b,
                         f"{item_b} B item read + {ent_b} B (key, sum) per merged term written"),
         "k_emit": (local_out * (ent_b + term_b),

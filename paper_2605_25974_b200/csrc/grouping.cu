@@ -93,16 +93,24 @@ __device__ bool deep_fit(const GCtx& G, int g, const uint16_t* lst, uint32_t cnt
   return true;
 }
 
-constexpr int kFitThreads = 256;  // batch terms per k_group_fit CTA (blockIdx.y = term block)
+// Two launch shapes, chosen on the device by the group count (the host never
+// reads it): THREADS = kGB, one CTA per 32 groups with every batch term (the
+// staged group chunks are shared by 1024 terms: best with many groups), or
+// THREADS = kFitThreads with blockIdx.y = term block (4x the CTAs: a few
+// hundred groups -- config 3: 23 words -- still fill the SMs).  Each launch
+// returns at once when the other shape applies.
+constexpr int kFitThreads = 256;
+constexpr int kFitSplitWords = 96;  // below this many 32-group words the split shape runs
 
-template <int W>
-__global__ void __launch_bounds__(kFitThreads) k_group_fit(GCtx G, int64_t b0, int bn) {
+template <int W, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_group_fit(GCtx G, int64_t b0, int bn) {
   constexpr int E = 128 * W;
   constexpr int GPC = 8;  // groups per shared-memory pass (8 KB x W)
   extern __shared__ u64 S[];  // [GPC][E]
   if (*G.overflow) return;
   const uint32_t G0 = *G.gcur;
-  const int t = blockIdx.y * kFitThreads + threadIdx.x;
+  if ((THREADS == kGB) == (((int64_t)G0 + 31) / 32 < kFitSplitWords)) return;
+  const int t = blockIdx.y * THREADS + threadIdx.x;
   const bool valid = t < bn;
   uint32_t off = 0, cnt = 0;
   if (valid) {
@@ -666,8 +674,10 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
     PLB_CHECK_LAUNCH("k_row_fill");
   }
   const size_t fit_smem = (size_t)8 * 128 * W * 8;
-  PLB_CUDA(cudaFuncSetAttribute(k_group_fit<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  PLB_CUDA(cudaFuncSetAttribute(k_group_fit<W, kGB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)fit_smem));
+  PLB_CUDA(cudaFuncSetAttribute(k_group_fit<W, kFitThreads>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fit_smem));
   PLB_CUDA(cudaFuncSetAttribute(k_group_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(ResolveSmem)));
   const size_t lists_smem = lists_smem_bytes<(W <= 8 ? W : 8)>();
@@ -697,9 +707,9 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
     }
     if (b0 > 0) {
       StageTimer t_(st, "k_group_fit");
-      // term blocks x group words: few groups (config 3: 23 words) still fill the SMs
-      k_group_fit<W><<<dim3((unsigned)fit_grid, kGB / kFitThreads), kFitThreads, fit_smem, st>>>(
-          G, b0, bn);
+      k_group_fit<W, kFitThreads><<<dim3((unsigned)fit_grid, kGB / kFitThreads), kFitThreads,
+                                    fit_smem, st>>>(G, b0, bn);
+      k_group_fit<W, kGB><<<fit_grid, kGB, fit_smem, st>>>(G, b0, bn);
     }
     {
       StageTimer t_(st, "k_group_firstk");
