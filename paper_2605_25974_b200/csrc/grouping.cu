@@ -57,6 +57,14 @@ struct GCtx {
   // chunk pool: ccap chunks of 128W uint64 + next links
   u64* pool;
   int32_t* cnext;
+  // chunk index of every group: linked blocks of 32 chunk ids in chunk order,
+  // so a warp tests 32 chunks of a big group per step (deep_fit_warp)
+  int32_t* tb_ids;                     // [tcap][32]
+  int32_t* tb_next;                    // [tcap]
+  int32_t* gtb_first;                  // gcap
+  int32_t* gtb_last;                   // gcap
+  int64_t tcap;
+  uint32_t* tb_pool_next;
   // scalars
   uint32_t* gcur;                      // groups so far
   uint32_t* pool_next;
@@ -78,19 +86,31 @@ struct GCtx {
 __device__ __forceinline__ int swap_entry(int e, int W) { return e < 64 * W ? e + 64 * W : e - 64 * W; }
 
 // ------------------------------------------------------------ fit tests
+// Does the term with entry list lst[0..cnt) commute with every member of group
+// g beyond its first chunk?  The whole warp walks the group's chunk index, 32
+// chunks per step (lane l XORs the term's entries of chunk 32b + l).  Round 1
+// walked the chunk list on the one thread that owned the term: a term
+// duplicating a member of a 10^4-member group (config 5 injects 10%
+// duplicates) kept one thread busy for ~150 dependent chunk visits while the
+// GPU idled (k_group_fit: 1.3% issue utilisation, 69% of config 5 grouping).
 template <int W>
-__device__ bool deep_fit(const GCtx& G, int g, const uint16_t* lst, uint32_t cnt) {
+__device__ __forceinline__ bool deep_fit_warp(const GCtx& G, int g, const uint16_t* lst,
+                                              uint32_t cnt, int nchunks) {
   constexpr int E = 128 * W;
-  int c = G.gfirst[g];
-  c = c >= 0 ? G.cnext[c] : -1;  // chunk 0 already tested
-  while (c >= 0) {
-    const u64* T = G.pool + (int64_t)c * E;
+  const int lane = threadIdx.x & 31;
+  int blk = G.gtb_first[g];
+  bool ok = true;
+  for (int o0 = 0; o0 < nchunks && ok && blk >= 0; o0 += 32) {
+    const int o = o0 + lane;
     u64 acc = 0;
-    for (uint32_t k = 0; k < cnt; ++k) acc ^= T[lst[k]];
-    if (acc) return false;
-    c = G.cnext[c];
+    if (o >= 1 && o < nchunks) {  // chunk 0 was tested from shared memory
+      const u64* T = G.pool + (int64_t)G.tb_ids[(int64_t)blk * 32 + lane] * E;
+      for (uint32_t k = 0; k < cnt; ++k) acc ^= T[lst[k]];
+    }
+    ok = !__any_sync(0xffffffffu, acc != 0ull);
+    blk = G.tb_next[blk];
   }
-  return true;
+  return ok;
 }
 
 // Two launch shapes, chosen on the device by the group count (the host never
@@ -135,6 +155,7 @@ __global__ void __launch_bounds__(THREADS) k_group_fit(GCtx G, int64_t b0, int b
         S[gi * E + e] = v;
       }
       __syncthreads();
+      uint32_t cand = 0;  // staged groups whose first chunk commutes with the term
       if (valid && g0 < G0) {
         u64 acc[GPC];
 #pragma unroll
@@ -144,14 +165,28 @@ __global__ void __launch_bounds__(THREADS) k_group_fit(GCtx G, int64_t b0, int b
 #pragma unroll
           for (int q = 0; q < GPC; ++q) acc[q] ^= S[q * E + e];
         }
-        uint32_t cand = 0;
 #pragma unroll
-        for (int q = 0; q < GPC; ++q) cand |= (acc[q] == 0 ? 1u : 0u) << q;
-        for (; cand; cand &= cand - 1) {  // rare: chunk 0 commutes
-          const int q = __ffs(cand) - 1;
-          const int64_t g = g0 + q;
-          if (g < G0 && (G.gsize[g] <= 64 || deep_fit<W>(G, (int)g, lst, cnt)))
+        for (int q = 0; q < GPC; ++q) cand |= (acc[q] == 0 && g0 + q < G0 ? 1u : 0u) << q;
+        for (uint32_t cb = cand; cb; cb &= cb - 1) {  // one-chunk groups are settled
+          const int q = __ffs(cb) - 1;
+          if (G.gsize[g0 + q] <= 64) {
             word |= 1u << (h * GPC + q);
+            cand &= ~(1u << q);
+          }
+        }
+      }
+      // larger groups: the warp takes the (term, group) pairs one at a time
+      for (unsigned pend = __ballot_sync(0xffffffffu, cand != 0u); pend;
+           pend = __ballot_sync(0xffffffffu, cand != 0u)) {
+        const int L = __ffs(pend) - 1;
+        const int q = __ffs(__shfl_sync(0xffffffffu, cand, L)) - 1;
+        const int g = (int)(g0 + q);
+        const uint32_t off_l = __shfl_sync(0xffffffffu, off, L);
+        const uint32_t cnt_l = __shfl_sync(0xffffffffu, cnt, L);
+        const bool fits = deep_fit_warp<W>(G, g, G.list + off_l, cnt_l, (int)((G.gsize[g] + 63) / 64));
+        if ((threadIdx.x & 31) == L) {
+          if (fits) word |= 1u << (h * GPC + q);
+          cand &= ~(1u << q);
         }
       }
       __syncthreads();
@@ -483,6 +518,20 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
       else G.cnext[prev] = id;
       prev = id;
       tab[k++] = id;
+      // chunk index: ordinal have + a of group g
+      const int ord = have + a;
+      if ((ord & 31) == 0) {
+        const int nb = (int)atomicAdd(G.tb_pool_next, 1u);
+        if ((int64_t)nb >= G.tcap) {
+          *G.overflow = 1;
+          break;
+        }
+        G.tb_next[nb] = -1;
+        if (ord == 0) G.gtb_first[g] = nb;
+        else G.tb_next[G.gtb_last[g]] = nb;
+        G.gtb_last[g] = nb;
+      }
+      G.tb_ids[(int64_t)G.gtb_last[g] * 32 + (ord & 31)] = id;
     }
     if (add > 0) G.glast[g] = prev;
     G.gsize[g] = (uint32_t)nw;
@@ -574,7 +623,7 @@ struct GLayout {
 static int64_t per_group_bytes(int W, int64_t gw_stride_per_group) {
   (void)gw_stride_per_group;
   return 4 * 4 /* gsize gfirst glast gpre */ + kGB / 8 /* fit0 bits */ +
-         (128LL * W * 8 + 4) /* one chunk */;
+         (128LL * W * 8 + 4) /* one chunk */ + 2 * 4 + 132 + 5 /* chunk index: ends, a block, id */;
 }
 
 static int64_t fixed_bytes(int W, int64_t M) {
@@ -625,6 +674,7 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
   G.gcur = scal;
   G.pool_next = scal + 1;
   G.overflow = scal + 2;
+  G.tb_pool_next = scal + 8;
   G.checks = (unsigned long long*)(scal + 4);
   // CSR entry lists of every term (same encoding as the bitmatrix)
   const unsigned nb = (unsigned)ceil_div(M, 256);
@@ -642,8 +692,8 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
   G.off = off;
   G.list = list;
   // remaining bytes -> group capacity
-  const int64_t rest = (int64_t)ws_bytes - o - 4096;
-  const int64_t chunk_bytes = 128LL * W * 8 + 4;
+  const int64_t rest = (int64_t)ws_bytes - o - 8192;
+  const int64_t chunk_bytes = 128LL * W * 8 + 4 + 5;  // chunk, link, share of an index block
   const int64_t member_chunks = (M + 63) / 64;
   int64_t gcap = (rest - member_chunks * chunk_bytes) / per_group_bytes(W, 0);
   if (gcap > M) gcap = M;
@@ -660,6 +710,11 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
   G.gpre = (uint32_t*)take(gcap * 4);
   G.fit0 = (uint32_t*)take((int64_t)kGB * G.gw_stride * 4);
   G.cnext = (int32_t*)take(G.ccap * 4);
+  G.tcap = G.ccap / 32 + gcap + 2;
+  G.tb_ids = (int32_t*)take(G.tcap * 32 * 4);
+  G.tb_next = (int32_t*)take(G.tcap * 4);
+  G.gtb_first = (int32_t*)take(gcap * 4);
+  G.gtb_last = (int32_t*)take(gcap * 4);
   G.pool = (u64*)take(G.ccap * 128LL * W * 8);
   if (o > (int64_t)ws_bytes) {
     set_error("pl_group_greedy: workspace layout overflow");
@@ -751,7 +806,7 @@ extern "C" int64_t pl_group_workspace_bytes(int W, int64_t M) {
   if (groups < 1024) groups = std::min<int64_t>(M, 1024);
   const int64_t chunks = (M + 63) / 64;
   return fixed_bytes(W, M) + a256(lists) + groups * per_group_bytes(W, 0) +
-         chunks * (128LL * W * 8 + 4) + 64 * 256;
+         chunks * (128LL * W * 8 + 4 + 5) + 64 * 256;
 }
 
 extern "C" int pl_group_greedy(int W, int64_t M, const uint64_t* x, const uint64_t* z,
