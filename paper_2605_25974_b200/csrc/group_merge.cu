@@ -6,87 +6,74 @@
 // every cross pair commutes, else open a new global group; pair_checks adds
 // |local| * |global group| for every global group tried (grouping.py:129-131).
 //
-// Per local group L (the sequence is inherently ordered, so one pair of
-// launches per local group, no host synchronisation in between):
-//   k_merge_anti  every term already placed (gid >= 0) is checked against L's
-//                 members (staged in shared memory, tiles of kMergeTile); an
-//                 anti-commuting pair marks the term's global group for this
-//                 epoch (anti_epoch[g] = epoch); a group already marked is
-//                 skipped.
-//   pick          the last CTA of k_merge_anti to finish (completion counter):
-//                 first unmarked group in creation order (or a new one), the
-//                 pair_checks contribution (|L| * sizes of the groups tried),
-//                 L's members joined to it -- one launch per local group.
+// The sequence is ordered, but the pair tests are not: local groups are taken
+// kMergeBatch at a time (K6's scheme at group granularity).
+//   k_merge_anti  every term already placed, and every term of the batch, is
+//                 checked against the batch's members (staged in shared memory
+//                 with their local-group index): an anti-commuting pair marks
+//                 bad[local][global group of the placed term] or, inside the
+//                 batch, cross[earlier local][later local].  A thread skips a
+//                 local group once its own group is marked for it.
+//   k_merge_pick  one CTA replays the batch in order: the first global group
+//                 not marked bad for the local group (bad also receives the
+//                 cross marks of batch groups already placed there), else a
+//                 new group; pair_checks; then the batch members' group ids.
+// Round 1 launched one marking kernel per local group (2,400 launches on
+// config 3 with 8 chunks, 28 ms, launch bound).
 #include "common.cuh"
 
 namespace plb {
 
 constexpr int kMergeThreads = 256;
-// L members per shared-memory tile (<= 16 KB of x/z words)
+constexpr int kMergeBatch = 256;  // local groups per batch
+// batch members per shared-memory tile (<= 16 KB of x/z words)
 __host__ __device__ constexpr int merge_tile(int W) { return W >= 8 ? 1024 / W : 256; }
 
-// first unmarked global group (or a new one) for local group `epoch`, the
-// pair_checks contribution, and the members joined to it (one CTA)
-__device__ void merge_pick(int32_t* __restrict__ gid, const int32_t* __restrict__ members,
-                           int64_t lo, int64_t hi, int32_t epoch,
-                           const int32_t* __restrict__ anti_epoch, int32_t* __restrict__ gsize,
-                           int32_t* __restrict__ n_global, int32_t* __restrict__ global_of_local,
-                           int64_t* __restrict__ pair_checks) {
-  __shared__ int32_t s_first;
-  __shared__ unsigned long long s_tried;
-  const int32_t G = *(volatile int32_t*)n_global;
-  if (threadIdx.x == 0) {
-    s_first = G;
-    s_tried = 0;
+// lg[t] = local group of term t (members lists the terms group by group)
+__global__ void k_merge_lgof(const int32_t* __restrict__ members, const int64_t* __restrict__ loff,
+                             int32_t n_local, int64_t M, int32_t* __restrict__ lg) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  int lo = 0, hi = n_local - 1;  // last l with loff[l] <= i
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (loff[mid] <= i) lo = mid;
+    else hi = mid - 1;
   }
-  __syncthreads();
-  for (int g = threadIdx.x; g < G; g += blockDim.x)
-    if (((volatile const int32_t*)anti_epoch)[g] != epoch) atomicMin(&s_first, g);
-  __syncthreads();
-  const int32_t first = s_first;
-  // groups tried: 0..first (inclusive) when one fits, all G otherwise
-  const int32_t last = first < G ? first : G - 1;
-  unsigned long long part = 0;
-  for (int g = threadIdx.x; g <= last; g += blockDim.x) part += (unsigned long long)gsize[g];
-  if (part) atomicAdd(&s_tried, part);
-  __syncthreads();
-  const int64_t L = hi - lo;
-  if (threadIdx.x == 0) {
-    *pair_checks += (int64_t)s_tried * L;
-    if (first == G) {
-      gsize[G] = 0;
-      *n_global = G + 1;
-    }
-    gsize[first] += (int32_t)L;
-    global_of_local[epoch] = first;
-  }
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) gid[members[i]] = first;
+  lg[members[i]] = lo;
 }
 
 template <int W>
 __global__ void __launch_bounds__(kMergeThreads)
 k_merge_anti(const u64* __restrict__ x, const u64* __restrict__ z, int64_t ld, int64_t M,
-             int32_t* __restrict__ gid, const int32_t* __restrict__ members, int64_t lo,
-             int64_t hi, int32_t epoch, int32_t* __restrict__ anti_epoch,
-             int32_t* __restrict__ gsize, int32_t* __restrict__ n_global,
-             int32_t* __restrict__ global_of_local, int64_t* __restrict__ pair_checks,
-             unsigned int* __restrict__ done) {
+             const int32_t* __restrict__ gid, const int32_t* __restrict__ lg,
+             const int32_t* __restrict__ members, int64_t lo, int64_t hi, int32_t l0,
+             uint8_t* bad, int64_t gstride, uint8_t* cross) {
   constexpr int kMergeTile = merge_tile(W);
   __shared__ u64 lx[W][kMergeTile], lz[W][kMergeTile];
+  __shared__ int32_t ll[kMergeTile];
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int32_t g = t < M ? gid[t] : -1;
-  bool live = g >= 0 && anti_epoch[g] != epoch;
+  const int32_t my = t < M ? lg[t] - l0 : -1;  // batch-local index of the term's own local group
+  const bool placed = g >= 0;
+  const bool inbatch = !placed && my >= 0 && my < kMergeBatch && t < M;
+  const bool role = placed || inbatch;
   u64 tx[W], tz[W];
 #pragma unroll
   for (int w = 0; w < W; ++w) {
-    tx[w] = live ? x[w * ld + t] : 0ull;
-    tz[w] = live ? z[w * ld + t] : 0ull;
+    tx[w] = role ? x[w * ld + t] : 0ull;
+    tz[w] = role ? z[w * ld + t] : 0ull;
   }
+  int cur = -1;      // batch-local group being scanned
+  bool skip = true;  // nothing left to learn about `cur`
+  volatile uint8_t* vbad = bad;
+  volatile uint8_t* vcross = cross;
   for (int64_t b = lo; b < hi; b += kMergeTile) {
     const int n = (int)(hi - b < kMergeTile ? hi - b : kMergeTile);
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const int64_t m = members[b + i];
+      ll[i] = lg[m] - l0;
 #pragma unroll
       for (int w = 0; w < W; ++w) {
         lx[w][i] = x[w * ld + m];
@@ -94,66 +81,111 @@ k_merge_anti(const u64* __restrict__ x, const u64* __restrict__ z, int64_t ld, i
       }
     }
     __syncthreads();
-    if (!__syncthreads_or(live)) continue;
-    if (live) {
-      bool anti = false;
-      for (int i = 0; i < n && !anti; ++i) {
-        u64 acc = 0;
-#pragma unroll
-        for (int w = 0; w < W; ++w) acc ^= (tx[w] & lz[w][i]) ^ (tz[w] & lx[w][i]);
-        anti = popc64(acc) & 1;
+    if (!role) continue;
+    for (int i = 0; i < n; ++i) {
+      const int L = ll[i];
+      if (L != cur) {  // next local group: anything to learn?
+        cur = L;
+        if (placed) skip = vbad[(int64_t)L * gstride + g] != 0;
+        else skip = my >= L || vcross[my * kMergeBatch + L] != 0;
       }
-      if (anti) {
-        anti_epoch[g] = epoch;
-        live = false;
+      if (skip) continue;
+      u64 acc = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) acc ^= (tx[w] & lz[w][i]) ^ (tz[w] & lx[w][i]);
+      if (popc64(acc) & 1) {
+        if (placed) vbad[(int64_t)L * gstride + g] = 1;
+        else vcross[my * kMergeBatch + L] = 1;
+        skip = true;
       }
     }
   }
-  // the last CTA to finish picks (no second launch per local group)
-  __shared__ bool s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  merge_pick(gid, members, lo, hi, epoch, anti_epoch, gsize, n_global, global_of_local,
-             pair_checks);
-  if (threadIdx.x == 0) *done = 0u;  // ready for the next local group
 }
 
+// One CTA replays local groups [l0, l1) in order.
 __global__ void __launch_bounds__(1024)
-k_merge_pick(int32_t* __restrict__ gid, const int32_t* __restrict__ members, int64_t lo,
-             int64_t hi, int32_t epoch, const int32_t* __restrict__ anti_epoch,
+k_merge_pick(int32_t* __restrict__ gid, const int32_t* __restrict__ lg,
+             const int32_t* __restrict__ members, const int64_t* __restrict__ loff, int32_t l0,
+             int32_t l1, uint8_t* bad, int64_t gstride, const uint8_t* __restrict__ cross,
              int32_t* __restrict__ gsize, int32_t* __restrict__ n_global,
              int32_t* __restrict__ global_of_local, int64_t* __restrict__ pair_checks) {
-  merge_pick(gid, members, lo, hi, epoch, anti_epoch, gsize, n_global, global_of_local,
-             pair_checks);
+  __shared__ int32_t s_first;
+  __shared__ unsigned long long s_tried;
+  __shared__ int32_t dest[kMergeBatch];
+  int32_t G = *n_global;
+  long long checks = 0;
+  for (int32_t l = l0; l < l1; ++l) {
+    const int b = l - l0;
+    if (threadIdx.x == 0) {
+      s_first = G;
+      s_tried = 0;
+    }
+    __syncthreads();
+    const uint8_t* row = bad + (int64_t)b * gstride;
+    int mine = G;  // this thread's first unmarked group (warp minimum, one atomic per warp)
+    for (int g = threadIdx.x; g < G && mine == G; g += blockDim.x)
+      if (row[g] == 0) mine = g;
+    mine = __reduce_min_sync(0xffffffffu, mine);
+    if ((threadIdx.x & 31) == 0 && mine < G) atomicMin(&s_first, mine);
+    __syncthreads();
+    const int32_t first = s_first;
+    // groups tried: 0..first (inclusive) when one fits, all G otherwise
+    const int32_t last = first < G ? first : G - 1;
+    unsigned int part = 0;  // (sizes sum to at most M < 2^31)
+    for (int g = threadIdx.x; g <= last; g += blockDim.x) part += (unsigned int)gsize[g];
+    part = __reduce_add_sync(0xffffffffu, part);
+    if ((threadIdx.x & 31) == 0 && part) atomicAdd(&s_tried, (unsigned long long)part);
+    __syncthreads();
+    const int64_t L = loff[l + 1] - loff[l];
+    checks += (long long)s_tried * L;
+    if (threadIdx.x == 0) {
+      if (first == G) gsize[G] = 0;
+      gsize[first] += (int32_t)L;
+      global_of_local[l] = first;
+      dest[b] = first;
+    }
+    if (first == G) ++G;
+    // later batch groups with an anti-commuting pair against this one cannot join `first`
+    for (int b2 = b + 1 + threadIdx.x; b2 < l1 - l0; b2 += blockDim.x)
+      if (cross[b * kMergeBatch + b2]) bad[(int64_t)b2 * gstride + first] = 1;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *n_global = G;
+    *pair_checks += checks;
+  }
+  for (int64_t i = loff[l0] + threadIdx.x; i < loff[l1]; i += blockDim.x) {
+    const int32_t t = members[i];
+    gid[t] = dest[lg[t] - l0];
+  }
 }
 
 template <int W>
 static int run_merge(int64_t M, const u64* x, const u64* z, int64_t ld, const int32_t* members,
                      const int64_t* local_off, int32_t n_local, int32_t* global_of_local,
                      int32_t* n_global, int64_t* pair_checks, void* ws, cudaStream_t st) {
+  // workspace: gid | lg | gsize | loff (device copy) | cross | bad
   int32_t* gid = (int32_t*)ws;
-  int32_t* anti_epoch = gid + M;
-  int32_t* gsize = anti_epoch + n_local;
-  unsigned int* done = (unsigned int*)(gsize + n_local);
-  PLB_CUDA(cudaMemsetAsync(gid, 0xFF, 4 * (size_t)M, st));           // -1: not placed yet
-  PLB_CUDA(cudaMemsetAsync(anti_epoch, 0xFF, 4 * (size_t)n_local, st));
+  int32_t* lg = gid + M;
+  int32_t* gsize = lg + M;
+  int64_t* loff = (int64_t*)(((uintptr_t)(gsize + n_local + 1) + 15) & ~(uintptr_t)15);
+  uint8_t* cross = (uint8_t*)(loff + n_local + 1);
+  uint8_t* bad = cross + (size_t)kMergeBatch * kMergeBatch;
+  const int64_t gstride = ((int64_t)n_local + 15) & ~(int64_t)15;  // a global group per local at most
+  PLB_CUDA(cudaMemsetAsync(gid, 0xFF, 4 * (size_t)M, st));  // -1: not placed yet
   PLB_CUDA(cudaMemsetAsync(n_global, 0, 4, st));
-  PLB_CUDA(cudaMemsetAsync(done, 0, 4, st));
-  const unsigned grid = (unsigned)ceil_div(M, kMergeThreads);
+  PLB_CUDA(cudaMemcpyAsync(loff, local_off, 8 * ((size_t)n_local + 1), cudaMemcpyHostToDevice, st));
+  if (n_local == 0) return PL_OK;
   StageTimer t_(st, "k_group_merge");
-  for (int32_t l = 0; l < n_local; ++l) {
-    const int64_t lo = local_off[l], hi = local_off[l + 1];
-    if (l > 0)  // marks, then its last CTA picks
-      k_merge_anti<W><<<grid, kMergeThreads, 0, st>>>(x, z, ld, M, gid, members, lo, hi, l,
-                                                      anti_epoch, gsize, n_global,
-                                                      global_of_local, pair_checks, done);
-    else
-      k_merge_pick<<<1, 1024, 0, st>>>(gid, members, lo, hi, l, anti_epoch, gsize, n_global,
-                                        global_of_local, pair_checks);
+  k_merge_lgof<<<(unsigned)ceil_div(M, 256), 256, 0, st>>>(members, loff, n_local, M, lg);
+  const unsigned grid = (unsigned)ceil_div(M, kMergeThreads);
+  for (int32_t l0 = 0; l0 < n_local; l0 += kMergeBatch) {
+    const int32_t l1 = std::min<int32_t>(n_local, l0 + kMergeBatch);
+    PLB_CUDA(cudaMemsetAsync(cross, 0, (size_t)kMergeBatch * kMergeBatch + (size_t)kMergeBatch * gstride, st));
+    k_merge_anti<W><<<grid, kMergeThreads, 0, st>>>(x, z, ld, M, gid, lg, members, local_off[l0],
+                                                    local_off[l1], l0, bad, gstride, cross);
+    k_merge_pick<<<1, 1024, 0, st>>>(gid, lg, members, loff, l0, l1, bad, gstride, cross, gsize,
+                                      n_global, global_of_local, pair_checks);
   }
   PLB_CHECK_LAUNCH("k_group_merge");
   return PL_OK;
@@ -164,7 +196,10 @@ static int run_merge(int64_t M, const u64* x, const u64* z, int64_t ld, const in
 using namespace plb;
 
 extern "C" int64_t pl_group_merge_workspace_bytes(int64_t M, int32_t n_local) {
-  return 4 * (M + 2 * (int64_t)n_local + 64);  // gid | anti_epoch | gsize | done
+  // gid | lg | gsize | loff | cross | bad (see run_merge)
+  const int64_t gstride = ((int64_t)n_local + 15) & ~(int64_t)15;
+  return 4 * (2 * M + (int64_t)n_local + 1) + 16 + 8 * ((int64_t)n_local + 1) +
+         (int64_t)plb::kMergeBatch * plb::kMergeBatch + (int64_t)plb::kMergeBatch * gstride + 256;
 }
 
 extern "C" int pl_group_merge(int W, int64_t M, const uint64_t* x, const uint64_t* z, int64_t ld,

@@ -172,19 +172,24 @@ def group_greedy_parallel(s, chunks: int, *, stats: GroupingStats | None = None
             results = list(pool.map(run_chunk, pieces))
     else:
         results = [run_chunk(p) for p in pieces]
+    # local groups in processing order (chunk order, creation order inside a
+    # chunk): members as one array, group by group, each in index order
+    mem_parts, size_parts = [], []
     for r0, gof, pc in results:
-        part = CommutationPartition.from_assignment(gof)
-        locals_.extend([[r0 + t for t in g] for g in part.groups])
+        gof = np.asarray(gof, dtype=np.int64)
+        mem_parts.append(r0 + np.argsort(gof, kind="stable"))
+        size_parts.append(np.bincount(gof))
         checks += pc
-    n_local = len(locals_)
+    sizes = np.concatenate(size_parts) if size_parts else np.zeros(0, np.int64)
+    n_local = int(sizes.shape[0])
     if n_local == 0:
         if stats is not None:
             stats.pair_checks += checks
         return CommutationPartition([], m)
-    members = torch.as_tensor(np.fromiter((t for g in locals_ for t in g), np.int32, m),
-                              device=dev)
+    mem_h = np.concatenate(mem_parts).astype(np.int32)
+    members = torch.as_tensor(mem_h, device=dev)
     off = np.zeros(n_local + 1, dtype=np.int64)
-    off[1:] = np.cumsum([len(g) for g in locals_])
+    off[1:] = np.cumsum(sizes)
     gol = torch.empty(n_local, dtype=torch.int32, device=dev)
     ng = torch.zeros(1, dtype=torch.int32, device=dev)
     pc = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -195,12 +200,15 @@ def group_greedy_parallel(s, chunks: int, *, stats: GroupingStats | None = None
                      off.ctypes.data, n_local, ptr(gol), ptr(ng), ptr(pc), ptr(ws), ws.numel(),
                      stream_ptr(dev))
     gol_h = gol.cpu().numpy()
-    groups: list[list[int]] = [[] for _ in range(int(ng.item()))]
-    for g, local in zip(gol_h, locals_):
-        groups[int(g)].extend(local)
+    # a global group is the concatenation of its local groups in processing
+    # order; chunks are increasing index ranges and two local groups of one
+    # chunk never share a global group, so that is ascending index order
+    gid = np.empty(m, dtype=np.int64)
+    gid[mem_h] = np.repeat(gol_h.astype(np.int64), sizes)
+    part = CommutationPartition.from_assignment(gid)
     if stats is not None:
         stats.pair_checks += checks + int(pc.item())
-    return CommutationPartition(groups, m)
+    return part
 
 
 def validate_partition(s, p: CommutationPartition) -> ValidationReport:
