@@ -468,10 +468,14 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
           G.tslot[i] = cslot;
         }
         __syncwarp();
-        for (unsigned m = okm; m; m &= m - 1) {  // BLOCKED[slot] |= the member's anti row
-          const int l = __ffs(m) - 1;
-          const int s = __shfl_sync(0xffffffffu, cslot, l);
-          R.blocked[s * kMaskLd + lane] |= R.aw[l * kMaskLd + lane];
+        if (done) {  // BLOCKED[slot] |= the member's anti row (words < j: terms already settled)
+          uint32_t* brow = R.blocked + cslot * kMaskLd;
+          const uint32_t* arow = R.aw + lane * kMaskLd;
+#pragma unroll 4
+          for (int w = j; w < kGAW; ++w) {  // independent atomics: the loop pipelines
+            const uint32_t v = arow[w];
+            if (v) atomicOr(&brow[w], v);
+          }
         }
         __syncwarp();
         todo &= ~okm;

@@ -329,6 +329,46 @@ def test_leaf_window_ties_fall_back(cuda):
     check_combined(out, R.combine(x, z, f, c))
 
 
+def test_level2_window_ties(cuda):
+    """Level 2 classifies on the 32 key bits after the bucket's shared prefix;
+    two far-apart clusters whose members differ only 48 bits further down give
+    every splitter of a cluster the same window, so every item takes the
+    full-key comparison against the tied splitters (and the leaves see long
+    shared prefixes)."""
+    r = np.random.default_rng(17)
+    m = 60_000
+    z = np.zeros((m, 1), np.uint64)
+    x = np.zeros((m, 1), np.uint64)
+    cluster = r.integers(0, 2, m).astype(np.uint64)
+    z[:, 0] = (cluster << np.uint64(63)) | r.integers(0, 1 << 16, m).astype(np.uint64)
+    f = r.integers(0, 4, m).astype(np.uint8)
+    c = (r.normal(size=m) + 1j * r.normal(size=m)).astype(np.complex128)
+    out = pl.sort_and_combine(soa(64, (x, z, f, c), cuda))
+    assert pl.sums.LAST_PLAN["n_buckets"] > 1 and pl.sums.LAST_PLAN["key_bits"] == 64
+    check_combined(out, R.combine(x, z, f, c))
+
+
+def test_distinct_leaves_with_dropped_terms(cuda):
+    """Leaves whose keys are all distinct are written straight from the rank
+    order unless a coefficient is dropped: zero operand coefficients (exact
+    zero products at eps = 0) and an eps that removes some single-item runs
+    send those leaves through the general path; both agree with the oracle."""
+    a, b = rng.config_columns(4, scale=0.06)                    # 600 x 600, ~all keys distinct
+    ac = a[3].copy()
+    ac[::7] = 0.0                                               # exact-zero products
+    a0 = (a[0], a[1], a[2], ac)
+    out = pl.sum_multiply(soa(500, a0, cuda), soa(500, b, cuda))
+    check_combined(out, R.outer_combine(*a0, *b))
+    assert len(out) < len(a[0]) * len(b[0])
+    eps = 0.3
+    out = pl.sum_multiply(soa(500, a, cuda), soa(500, b, cuda), eps=eps)
+    exp = R.outer_combine(*a, *b, eps=eps)
+    check_combined(out, exp)
+    assert 0 < len(out) < len(a[0]) * len(b[0])
+    keep_all = pl.sum_multiply(soa(500, a0, cuda), soa(500, b, cuda), eps=-1.0)
+    assert len(keep_all) == len(R.outer_combine(*a0, *b, eps=-1.0)[3])
+
+
 def test_eps_drop_large(cuda):
     """eps drops on a 10^6-product outer product (strict > eps keeps)."""
     a, b = rng.config_columns(2)
