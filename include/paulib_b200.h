@@ -63,6 +63,17 @@ int pl_batch_sip(int W, int64_t P,
                  const uint64_t* bx, const uint64_t* bz, int64_t ldb,
                  uint8_t* anti, void* stream);
 
+/* One pair from HOST memory (the scalar API: PauliString.multiply,
+ * strings.py:133-137, and symplectic_inner_product / commutes, :141-147):
+ * o = a * b with o.k = (ak + bk + phase(a, b)) mod 4, and *anti = 1 when a and
+ * b anti-commute.  ax..bz and ox, oz are HOST arrays of W words; ox, oz, ok and
+ * anti may be NULL.  The operands travel through a mapped pinned buffer the
+ * kernel reads and writes directly: one launch and one synchronisation of
+ * `stream` per call (the call returns with the results in place). */
+int pl_pair_host(int W, const uint64_t* ax, const uint64_t* az, int ak,
+                 const uint64_t* bx, const uint64_t* bz, int bk,
+                 uint64_t* ox, uint64_t* oz, int* ok, int* anti, void* stream);
+
 /* ------------------------------------------------------------------------
  * K2 raw — outer product without combine.  Replaces sums.py:144-174
  * (_multiply_columns) + sums.py:123-141 (_multiply_block): output row

@@ -57,6 +57,7 @@ SIGNATURES = {
     "pl_abi_version": (_I, []),
     "pl_batch_multiply": (_I, [_I, _L, _P, _P, _P, _L, _P, _P, _P, _L, _P, _P, _P, _L, _P]),
     "pl_batch_sip": (_I, [_I, _L, _P, _P, _L, _P, _P, _L, _P, _P]),
+    "pl_pair_host": (_I, [_I, _P, _P, _I, _P, _P, _I, _P, _P, _P, _P, _P]),
     "pl_outer_multiply_raw": (_I, [_I, _L, _L, _P, _P, _P, _P, _L, _P, _P, _P, _P, _L,
                                    _P, _P, _P, _P, _L, _P]),
     "pl_outer_plan": (_I, [_I, _L, _L, _P, _P, _L, _P, _P, _L, C.POINTER(MergePlan), _P]),

@@ -5,6 +5,8 @@
 // W=8).  Each thread owns two adjacent pairs so every plane access is one
 // 128-bit load/store, coalesced across the warp.
 #include "common.cuh"
+#include <cstring>
+#include <mutex>
 
 namespace plb {
 
@@ -233,4 +235,86 @@ extern "C" int pl_outer_multiply_raw(int W, int64_t Ma, int64_t Mb, const uint64
   return PLB_DISPATCH_W(W, launch_outer_raw, Ma, Mb, (const u64*)ax, (const u64*)az, ak, ac, lda,
                         (const u64*)bx, (const u64*)bz, bk, bc, ldb, (u64*)ox, (u64*)oz, ok, oc,
                         ldo, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------------
+// One pair from HOST memory: product and symplectic parity in one launch.
+// The scalar API (PauliString.multiply / commutes, strings.py:133-147) used to
+// move six one-element tensors to the device per call (~100 us); here the
+// operands sit in a mapped pinned buffer the kernel reads and writes directly
+// (zero-copy), so a call costs one launch and one stream synchronisation.
+namespace plb {
+
+constexpr int kPairMaxW = 16;
+// mapped buffer layout (u64 words): in ax | az | bx | bz | ka, kb ; out x | z | k, sip
+constexpr int kPairIn = 4 * kPairMaxW + 2, kPairOut = 2 * kPairMaxW + 2;
+
+__global__ void __launch_bounds__(32) k_pair_host(int W, const u64* __restrict__ in,
+                                                  u64* __restrict__ out) {
+  const int lane = threadIdx.x;
+  const bool on = lane < W;
+  const u64 ax = on ? in[lane] : 0ull, az = on ? in[kPairMaxW + lane] : 0ull;
+  const u64 bx = on ? in[2 * kPairMaxW + lane] : 0ull, bz = on ? in[3 * kPairMaxW + lane] : 0ull;
+  int ph = phase_word(ax, az, bx, bz);
+  int sp = popc64(sip_word(ax, az, bx, bz));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ph += __shfl_xor_sync(0xffffffffu, ph, o);
+    sp += __shfl_xor_sync(0xffffffffu, sp, o);
+  }
+  if (on) {
+    out[lane] = ax ^ bx;
+    out[kPairMaxW + lane] = az ^ bz;
+  }
+  if (lane == 0) {
+    out[2 * kPairMaxW] = (u64)(((int)in[4 * kPairMaxW] + (int)in[4 * kPairMaxW + 1] + ph) & 3);
+    out[2 * kPairMaxW + 1] = (u64)(sp & 1);
+  }
+}
+
+}  // namespace plb
+
+extern "C" int pl_pair_host(int W, const uint64_t* ax, const uint64_t* az, int ak,
+                            const uint64_t* bx, const uint64_t* bz, int bk, uint64_t* ox,
+                            uint64_t* oz, int* ok, int* anti, void* stream) {
+  using namespace plb;
+  if (!valid_words(W)) {
+    set_error("unsupported word count W=%d", W);
+    return PL_ERR_TIER;
+  }
+  if (!ax || !az || !bx || !bz) {
+    set_error("pl_pair_host: operand pointers must not be NULL");
+    return PL_ERR_ARG;
+  }
+  static std::mutex mtx;
+  static u64* hbuf[64] = {nullptr};
+  static u64* dbuf[64] = {nullptr};
+  int dev = 0;
+  PLB_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) {
+    set_error("device index %d out of range", dev);
+    return PL_ERR_ARG;
+  }
+  std::lock_guard<std::mutex> lock(mtx);
+  if (!hbuf[dev]) {
+    PLB_CUDA(cudaHostAlloc((void**)&hbuf[dev], (kPairIn + kPairOut) * sizeof(u64), cudaHostAllocMapped));
+    PLB_CUDA(cudaHostGetDevicePointer((void**)&dbuf[dev], hbuf[dev], 0));
+  }
+  u64* h = hbuf[dev];
+  memcpy(h, ax, 8 * W);
+  memcpy(h + kPairMaxW, az, 8 * W);
+  memcpy(h + 2 * kPairMaxW, bx, 8 * W);
+  memcpy(h + 3 * kPairMaxW, bz, 8 * W);
+  h[4 * kPairMaxW] = (u64)(ak & 3);
+  h[4 * kPairMaxW + 1] = (u64)(bk & 3);
+  cudaStream_t st = (cudaStream_t)stream;
+  k_pair_host<<<1, 32, 0, st>>>(W, dbuf[dev], dbuf[dev] + kPairIn);
+  PLB_CHECK_LAUNCH("k_pair_host");
+  PLB_CUDA(cudaStreamSynchronize(st));
+  const u64* o = h + kPairIn;
+  if (ox) memcpy(ox, o, 8 * W);
+  if (oz) memcpy(oz, o + kPairMaxW, 8 * W);
+  if (ok) *ok = (int)o[2 * kPairMaxW];
+  if (anti) *anti = (int)o[2 * kPairMaxW + 1];
+  return PL_OK;
 }

@@ -140,30 +140,37 @@ def _dev_planes(words: np.ndarray, dev) -> torch.Tensor:
     return u64_to_i64_tensor(np.ascontiguousarray(words.reshape(-1, 1))).to(dev)
 
 
-def _pair_multiply(ax, az, ak, bx, bz, bk):
+def _host_words(v) -> np.ndarray:
+    return np.ascontiguousarray(v, dtype=np.uint64)
+
+
+def _pair_host(ax, az, ak, bx, bz, bk, want_product: bool):
+    """One launch of ``pl_pair_host``: (x, z, k) of a*b, or the anti-commutation bit."""
+    import ctypes as C
+
     dev = cuda_device()
+    ax, az, bx, bz = (_host_words(v) for v in (ax, az, bx, bz))
     W = ax.shape[0]
-    t_ax, t_az, t_bx, t_bz = (_dev_planes(v, dev) for v in (ax, az, bx, bz))
-    t_ak = torch.tensor([ak], dtype=torch.uint8, device=dev)
-    t_bk = torch.tensor([bk], dtype=torch.uint8, device=dev)
-    ox = torch.empty((W, 1), dtype=torch.int64, device=dev)
-    oz = torch.empty_like(ox)
-    ok = torch.empty(1, dtype=torch.uint8, device=dev)
     with torch.cuda.device(dev):
-        _native.call("pl_batch_multiply", W, 1, ptr(t_ax), ptr(t_az), ptr(t_ak), 1, ptr(t_bx),
-                     ptr(t_bz), ptr(t_bk), 1, ptr(ox), ptr(oz), ptr(ok), 1, stream_ptr(dev))
-    return i64_tensor_to_u64(ox)[:, 0], i64_tensor_to_u64(oz)[:, 0], int(ok.item())
+        if want_product:
+            ox, oz = np.empty(W, np.uint64), np.empty(W, np.uint64)
+            ok = C.c_int(0)
+            _native.call("pl_pair_host", W, ax.ctypes.data, az.ctypes.data, int(ak),
+                         bx.ctypes.data, bz.ctypes.data, int(bk), ox.ctypes.data, oz.ctypes.data,
+                         C.addressof(ok), None, stream_ptr(dev))
+            return ox, oz, int(ok.value)
+        anti = C.c_int(0)
+        _native.call("pl_pair_host", W, ax.ctypes.data, az.ctypes.data, 0, bx.ctypes.data,
+                     bz.ctypes.data, 0, None, None, None, C.addressof(anti), stream_ptr(dev))
+        return int(anti.value)
+
+
+def _pair_multiply(ax, az, ak, bx, bz, bk):
+    return _pair_host(ax, az, ak, bx, bz, bk, True)
 
 
 def _pair_sip(ax, az, bx, bz) -> int:
-    dev = cuda_device()
-    W = ax.shape[0]
-    t_ax, t_az, t_bx, t_bz = (_dev_planes(v, dev) for v in (ax, az, bx, bz))
-    out = torch.empty(1, dtype=torch.uint8, device=dev)
-    with torch.cuda.device(dev):
-        _native.call("pl_batch_sip", W, 1, ptr(t_ax), ptr(t_az), 1, ptr(t_bx), ptr(t_bz), 1,
-                     ptr(out), stream_ptr(dev))
-    return int(out.item())
+    return _pair_host(ax, az, 0, bx, bz, 0, False)
 
 
 def batch_multiply(ax, az, ak, bx, bz, bk):
