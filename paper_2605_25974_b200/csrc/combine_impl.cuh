@@ -599,6 +599,22 @@ static inline size_t sample_smem_bytes(int ns, int KW) {
   return (size_t)ns * 8 * KW + (size_t)pow2_ceil(ns) * 8 + 16;
 }
 
+// level-1 prefix table: tab[h] = number of splitters whose top kTabBits bits
+// are < h (h = 0 .. 2^kTabBits); a key with prefix h lies after splitter
+// tab[h]-1 and before splitter tab[h+1], so only [tab[h], tab[h+1]) is searched
+__device__ __forceinline__ void l1_table_fill(const Dims& D, const Ctl& C, int first, int stride) {
+  const int nsp = D.nb1 - 1;
+  for (int h = first; h <= (1 << kTabBits); h += stride) {
+    int lo = 0, hi = nsp;  // first splitter with prefix >= h
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((int64_t)(C.split[mid] >> (64 - kTabBits)) < (int64_t)h) lo = mid + 1;
+      else hi = mid;
+    }
+    C.l1tab[h] = (uint16_t)lo;
+  }
+}
+
 // ------------------------------------------------------------- 1. sampler
 // One CTA: ns deterministic sample keys of the product (raw rows spread
 // evenly), sorted, every (ns/nb1)-th taken as a level-1 splitter.  The sort
@@ -636,24 +652,9 @@ k_sample(Layout L, Dims D, SrcA S, Ctl C) {
 #pragma unroll
     for (int d = 0; d < KW; ++d) C.split[d * D.nb1 + (b - 1)] = K[d * ns + src];
   }
-}
-
-// level-1 prefix table: tab[h] = number of splitters whose top kTabBits bits
-// are < h (h = 0 .. 2^kTabBits); a key with prefix h lies after splitter
-// tab[h]-1 and before splitter tab[h+1], so only [tab[h], tab[h+1]) is searched
-template <int KW>
-__global__ void k_l1_table(Dims D, Ctl C) {
-  const int nsp = D.nb1 - 1;
-  for (int h = blockIdx.x * blockDim.x + threadIdx.x; h <= (1 << kTabBits);
-       h += gridDim.x * blockDim.x) {
-    int lo = 0, hi = nsp;  // first splitter with prefix >= h
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if ((int64_t)(C.split[mid] >> (64 - kTabBits)) < (int64_t)h) lo = mid + 1;
-      else hi = mid;
-    }
-    C.l1tab[h] = (uint16_t)lo;
-  }
+  // level-1 prefix table in the same launch (the splitters are this CTA's own writes)
+  __syncthreads();
+  l1_table_fill(D, C, threadIdx.x, blockDim.x);
 }
 
 // ---------------------------------------------------- 2./4. count, scatter
@@ -669,11 +670,10 @@ __global__ void k_l1_table(Dims D, Ctl C) {
 // shared memory, so no divergent per-segment loops), a 64-bit accumulator
 // flushed into the key words by a static select.
 template <int W, int KW>
-__device__ __forceinline__ void pack_sparse(const Layout& L, const u64* seg, u64 (&key)[KW]) {
+__device__ __forceinline__ void pack_sparse(const Layout& L, const u64 (&seg)[2 * W],
+                                            u64 (&key)[KW]) {
 #pragma unroll
   for (int d = 0; d < KW; ++d) key[d] = 0;
-  int s = 0;
-  u64 w = seg[0];
   u64 acc = 0;
   int fill = 0, wi = 0;  // bits in acc, key word being filled
   auto flush = [&](u64 v) {
@@ -682,23 +682,27 @@ __device__ __forceinline__ void pack_sparse(const Layout& L, const u64* seg, u64
       if (d == wi) key[d] = v;
     ++wi;
   };
-  for (;;) {
-    while (w == 0 && s < 2 * W - 1) w = seg[++s];
-    if (w == 0) break;
-    const int hb = 63 - __clzll((long long)w);
-    w ^= 1ull << hb;
-    const int p = L.pos[s] + (L.len[s] - 1 - hb);
-    const u64 v = (u64)(L.key_bits - p);
-    const int nb = L.sbits;
-    if (fill + nb < 64) {
-      acc |= v << (64 - fill - nb);
-      fill += nb;
-    } else {
-      const int r = fill + nb - 64;  // bits spilling into the next word
-      acc |= v >> r;
-      flush(acc);
-      acc = r ? v << (64 - r) : 0ull;
-      fill = r;
+  const int nb = L.sbits;
+  // the segments in order (a uniform, unrolled loop: the words stay in
+  // registers), each from its high bit down
+#pragma unroll
+  for (int s = 0; s < 2 * W; ++s) {
+    u64 w = seg[s];
+    const int top = L.key_bits - (L.pos[s] + L.len[s] - 1);  // value of the segment's bit 0 ... + hb
+    while (w) {
+      const int hb = 63 - __clzll((long long)w);
+      w ^= 1ull << hb;
+      const u64 v = (u64)(top + hb);  // = key_bits - p with p = pos + (len - 1 - hb)
+      if (fill + nb < 64) {
+        acc |= v << (64 - fill - nb);
+        fill += nb;
+      } else {
+        const int r = fill + nb - 64;  // bits spilling into the next word
+        acc |= v >> r;
+        flush(acc);
+        acc = r ? v << (64 - r) : 0ull;
+        fill = r;
+      }
     }
   }
   if (fill && wi < KW) flush(acc);  // the zero terminator is the zero tail
@@ -708,20 +712,18 @@ template <int W, int KW, int MODE>
 __global__ void __launch_bounds__(256) k_pack_ops(Layout L, SrcA S, int64_t ma, int64_t mb, Ctl C) {
   const int64_t n = ma + (MODE == 0 ? mb : 0);
   if constexpr (MODE == 1 && W <= 8) if (L.sparse) {
-    __shared__ u64 segs[256][2 * W + 1];
-    u64* seg = segs[threadIdx.x];
     for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x; t0 < n; t0 += (int64_t)gridDim.x * blockDim.x) {
       const int64_t t = t0 + threadIdx.x;
       if (t < n) {
         int base = S.ak ? S.ak[t] : 0;
+        u64 seg[2 * W];
 #pragma unroll
-        for (int q = 0; q < 2 * W; ++q) {
+        for (int q = 0; q < 2 * W; ++q) {  // all plane loads in flight together
           const int w = q < W ? q : q - W;
-          const int len = L.len[q];
-          u64 v = 0;
-          if (len) v = (((q < W ? S.az : S.ax)[w * S.lda + t]) >> L.lo[q]) & low_mask(len);
-          seg[q] = v;
+          seg[q] = L.len[q] ? (q < W ? S.az : S.ax)[w * S.lda + t] : 0ull;
         }
+#pragma unroll
+        for (int q = 0; q < 2 * W; ++q) seg[q] = (seg[q] >> L.lo[q]) & low_mask(L.len[q]);
         u64 key[KW];
         pack_sparse<W, KW>(L, seg, key);
 #pragma unroll
@@ -1841,11 +1843,6 @@ static int run_pipeline(const pl_merge_plan& P, const SrcA& S0, void* ws, const 
     k_sample<W, KW, MODE><<<1, kLeafThreads, sm1, st>>>(L, D, S, C);
     PLB_CHECK_LAUNCH("k_sample");
   }
-  {
-    StageTimer t_(st, "k_l1_table");
-    k_l1_table<KW><<<((1 << kTabBits) + 256) / 256, 256, 0, st>>>(D, C);
-    PLB_CHECK_LAUNCH("k_l1_table");
-  }
   const size_t gsm = gen_smem_bytes(W, KW, D.nb1);
   dim3 ggrid;
   if (MODE == 0) ggrid = dim3((unsigned)ceil_div(D.ma, kTileA), (unsigned)ceil_div(D.mb, kTileB));
@@ -1981,11 +1978,6 @@ static int run_partition(const pl_merge_plan& P, const SrcA& S, int64_t j0, int6
       StageTimer t_(st, "k_sample");
       k_sample<W, KW, 0><<<1, kLeafThreads, sm1, st>>>(L, D, S, C);
       PLB_CHECK_LAUNCH("k_sample");
-    }
-    {
-      StageTimer t_(st, "k_l1_table");
-      k_l1_table<KW><<<((1 << kTabBits) + 256) / 256, 256, 0, st>>>(D, C);
-      PLB_CHECK_LAUNCH("k_l1_table");
     }
     const size_t gsm = gen_smem_bytes(W, KW, D.nb1);
     const dim3 ggrid((unsigned)ceil_div(D.ma, kTileA), (unsigned)ceil_div(D.mb, kTileB));

@@ -834,10 +834,44 @@ __global__ void k_range_map(Dims D, Ctl C) {
   for (uint32_t r = (pre + T - 1) / T; r * T < pre + k; ++r) C.rmap[r] = l;
 }
 
+// Small merges (<= kScanSmallLeaves leaf slots): the scan of the kept counts,
+// its total and the range map in ONE single-CTA launch instead of four (the
+// three-kernel scan + k_range_map); a 10^6-item merge is bound by its ~15
+// dependent launches, not by bandwidth.
+constexpr int kScanSmallItems = 16;
+constexpr int kScanSmallLeaves = 1024 * kScanSmallItems;
+
+template <int KW>
+__global__ void __launch_bounds__(1024) k_leaf_scan_small(Dims D, Ctl C) {
+  constexpr uint32_t T = emit_tile(KW);
+  const uint32_t n_leaves = *C.n_leaves;
+  const int base = threadIdx.x * kScanSmallItems;
+  uint32_t v[kScanSmallItems];
+  uint32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanSmallItems; ++k) {
+    const int l = base + k;
+    v[k] = l < D.max_leaves ? C.kept[l] : 0u;  // (leaf slots past n_leaves hold 0)
+    s += v[k];
+  }
+  uint32_t total;
+  uint32_t pre = block_excl_scan(s, &total);
+  if (threadIdx.x == 0) *C.scan_total = total;
+#pragma unroll
+  for (int k = 0; k < kScanSmallItems; ++k) {
+    const int l = base + k;
+    if (l < D.max_leaves) C.kprefix[l] = pre;
+    if ((uint32_t)l < n_leaves && v[k])
+      for (uint32_t r = (pre + T - 1) / T; r * T < pre + v[k]; ++r) C.rmap[r] = (uint32_t)l;
+    pre += v[k];
+  }
+}
+
 template <int W, int KW>
 __global__ void __launch_bounds__(kEmitThreads)
 k_emit(Layout L, Dims D, Ctl C, OutP O) {
   constexpr int T = emit_tile(KW);
+  constexpr int TM = T;  // granularity of the range map
   constexpr int PER = T / kEmitThreads;
   extern __shared__ u64 sm[];
   u64* KS = sm;                                              // [KW][T]
@@ -866,9 +900,9 @@ k_emit(Layout L, Dims D, Ctl C, OutP O) {
     const bool bulk = bulk_ok && o1 - (uint32_t)o0 == (uint32_t)T;
     if (tid == 0) bulk_wait_read_all();  // previous tile's bulk stores done reading KS/SS/PB
     __syncthreads();
-    const uint32_t r = (uint32_t)(o0 / T);
-    const uint32_t l0 = C.rmap[r];
-    const uint32_t l1 = o1 < total ? C.rmap[r + 1] : n_leaves - 1;
+    const uint32_t l0 = C.rmap[(uint32_t)(o0 / TM)];
+    const uint64_t rl = (uint64_t)(o1 - 1) / TM + 1;  // first range-map block past the tile
+    const uint32_t l1 = rl * TM < total ? C.rmap[rl] : n_leaves - 1;
     for (uint32_t lb = l0; lb <= l1; lb += kEmitThreads) {
       const uint32_t nl = l1 - lb + 1 < (uint32_t)kEmitThreads ? l1 - lb + 1 : (uint32_t)kEmitThreads;
       if (tid < (int)nl) {
@@ -980,12 +1014,16 @@ static int launch_leaves(const Layout& L, const Dims& D, const SrcA& S, const Ct
     ks<<<(unsigned)D.max_leaves, kLeafThreads2, lsm, st>>>(L, D, S, C, O.eps);
     PLB_CHECK_LAUNCH("k_leaf_sort");
   }
-  {
-    StageTimer t_(st, "k_leaf_scan");
-    int rc = exclusive_scan_u32(C.kept, C.kprefix, D.max_leaves, C.scan_scratch, C.scan_total, st);
-    if (rc) return rc;
-  }
-  {
+  if (D.max_leaves <= kScanSmallLeaves) {
+    StageTimer t_(st, "k_leaf_scan_small");
+    k_leaf_scan_small<KW><<<1, 1024, 0, st>>>(D, C);
+    PLB_CHECK_LAUNCH("k_leaf_scan_small");
+  } else {
+    {
+      StageTimer t_(st, "k_leaf_scan");
+      int rc = exclusive_scan_u32(C.kept, C.kprefix, D.max_leaves, C.scan_scratch, C.scan_total, st);
+      if (rc) return rc;
+    }
     StageTimer t_(st, "k_range_map");
     k_range_map<KW><<<(unsigned)ceil_div(D.max_leaves, 256), 256, 0, st>>>(D, C);
     PLB_CHECK_LAUNCH("k_range_map");
