@@ -116,11 +116,11 @@ __device__ __forceinline__ unsigned long long lds64(uint32_t addr) {
 
 // --------------------------------------------- method 1, generic lists
 template <int W>
-__global__ void __launch_bounds__(1024, 1)
-k_bitmatrix_lists(const u64* __restrict__ x, const u64* __restrict__ z, int64_t ld, int64_t M,
-                  int64_t row0, int64_t rows, int64_t col0, int64_t cols,
-                  const uint32_t* __restrict__ off, const uint16_t* __restrict__ list,
-                  uint32_t* __restrict__ bits, int64_t ld_bits, int64_t rows_per_split) {
+__device__ __forceinline__ void bitmatrix_lists_body(
+    const u64* __restrict__ x, const u64* __restrict__ z, int64_t ld, int64_t M, int64_t row0,
+    int64_t rows, int64_t col0, int64_t cols, const uint32_t* __restrict__ off,
+    const uint16_t* __restrict__ list, uint32_t* __restrict__ bits, int64_t ld_bits,
+    int64_t rows_per_split) {
   constexpr int E = 128 * W;
   constexpr int TS = E + kTPad;
   extern __shared__ uint32_t T[];  // [32][TS]
@@ -145,6 +145,16 @@ k_bitmatrix_lists(const u64* __restrict__ x, const u64* __restrict__ z, int64_t 
     }
     if (lane < words_here) bits[i * ld_bits + wcol + lane] = acc;
   }
+}
+
+template <int W>
+__global__ void __launch_bounds__(1024, 1)
+k_bitmatrix_lists(const u64* __restrict__ x, const u64* __restrict__ z, int64_t ld, int64_t M,
+                  int64_t row0, int64_t rows, int64_t col0, int64_t cols,
+                  const uint32_t* __restrict__ off, const uint16_t* __restrict__ list,
+                  uint32_t* __restrict__ bits, int64_t ld_bits, int64_t rows_per_split) {
+  bitmatrix_lists_body<W>(x, z, ld, M, row0, rows, col0, cols, off, list, bits, ld_bits,
+                          rows_per_split);
 }
 
 // ------------------- method 1, letter slices (fast path)

@@ -617,6 +617,25 @@ __global__ void __launch_bounds__(1024) k_group_prefix(GCtx G, uint32_t* g0_out)
   }
 }
 
+// Intra-batch anti rows of up to kAntiSuper consecutive batches in one launch
+// (blockIdx.z = batch): they do not depend on the grouping state, and one
+// batch alone (4 CTAs) leaves the GPU idle (config 3: 33 us per batch, 98
+// launches; config 5: 65 ms of 593).
+constexpr int kAntiSuper = 64;
+
+template <int W>
+__global__ void __launch_bounds__(1024, 1)
+k_group_anti_batches(const u64* __restrict__ x, const u64* __restrict__ z, int64_t ld, int64_t M,
+                     int64_t b_first, const uint32_t* __restrict__ off,
+                     const uint16_t* __restrict__ list, uint32_t* __restrict__ anti_all) {
+  const int64_t b0 = b_first + (int64_t)blockIdx.z * kGB;
+  if (b0 >= M) return;
+  const int64_t bn = M - b0 < kGB ? M - b0 : kGB;
+  if ((int64_t)blockIdx.y * 256 >= bn) return;
+  bitmatrix_lists_body<W>(x, z, ld, M, b0, bn, b0, bn, off + b0, list,
+                          anti_all + (int64_t)blockIdx.z * kGB * kGAW, kGAW, 256);
+}
+
 // ------------------------------------------------------------ host side
 static inline int64_t a256(int64_t v) { return (v + 255) & ~(int64_t)255; }
 
@@ -636,7 +655,7 @@ static int64_t fixed_bytes(int W, int64_t M) {
   o += a256((M + 1) * 4);                       // off
   o += a256(scan_scratch_words(M) * 4);         // scan scratch
   o += a256(64);                                // scalars
-  o += a256((int64_t)kGB * kGK * 4) + a256(kGB * 4) + a256((int64_t)kGB * kGAW * 4);
+  o += a256((int64_t)kGB * kGK * 4) + a256(kGB * 4) + a256((int64_t)kAntiSuper * kGB * kGAW * 4);
   o += a256(kGB * 4) * 3 + a256((int64_t)kGB * kSlotChunks * 4);
   o += a256(16);                                // g0 snapshot
   return o;
@@ -664,7 +683,8 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
   uint32_t* scal = (uint32_t*)take(64);
   G.fitk = (int32_t*)take((int64_t)kGB * kGK * 4);
   G.nfit = (int32_t*)take(kGB * 4);
-  G.anti = (uint32_t*)take((int64_t)kGB * kGAW * 4);
+  uint32_t* anti_all = (uint32_t*)take((int64_t)kAntiSuper * kGB * kGAW * 4);
+  G.anti = anti_all;
   G.member = (uint32_t*)take(kGB * 4);
   G.tslot = (int32_t*)take(kGB * 4);
   G.slot_old = (int32_t*)take(kGB * 4);
@@ -741,7 +761,7 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
                                 (int)sizeof(ResolveSmem)));
   const size_t lists_smem = lists_smem_bytes<(W <= 8 ? W : 8)>();
   if (W <= 8) {
-    PLB_CUDA(cudaFuncSetAttribute(k_bitmatrix_lists<W>,
+    PLB_CUDA(cudaFuncSetAttribute(k_group_anti_batches<(W <= 8 ? W : 8)>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lists_smem));
   }
   const int fit_grid = 2 * num_sms();
@@ -751,13 +771,19 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
       StageTimer t_(st, "k_group_prefix");
       k_group_prefix<<<1, 1024, 0, st>>>(G, g0snap);
     }
-    {
+    if (W <= 8) {
+      const int64_t bi = (b0 / kGB) % kAntiSuper;  // batch inside the super-batch
+      G.anti = anti_all + bi * kGB * kGAW;
+      if (bi == 0) {
+        StageTimer t_(st, "k_group_anti");
+        const int64_t nbatch = std::min<int64_t>(kAntiSuper, ceil_div(M - b0, (int64_t)kGB));
+        k_group_anti_batches<(W <= 8 ? W : 8)><<<dim3(1, kGB / 256, (unsigned)nbatch), 1024,
+                                                 lists_smem, st>>>(x, z, ld, M, b0, off, list,
+                                                                   anti_all);
+      }
+    } else {
       StageTimer t_(st, "k_group_anti");
-      if (W <= 8) {
-        dim3 grid(1, (unsigned)ceil_div(bn, 256));
-        k_bitmatrix_lists<W><<<grid, 1024, lists_smem, st>>>(x, z, ld, M, b0, bn, b0, bn,
-                                                             off + b0, list, G.anti, kGAW, 256);
-      } else {
+      {
         constexpr int kDC = DirectCols<W>::value;
         dim3 grid((unsigned)ceil_div(bn, kDC), (unsigned)ceil_div(bn, kDirectRows));
         k_bitmatrix_direct<W><<<grid, kDirectRows, 0, st>>>(x, z, ld, M, b0, bn, b0, bn, G.anti,

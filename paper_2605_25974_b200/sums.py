@@ -479,6 +479,11 @@ def _remember(plan) -> None:
 
 
 LAST_D2H_BYTES = 0  # instrumentation: bytes the most recent _download copied from the device
+# Rates (GB/s) of a pinned D2H copy and of a host clear of pinned memory while
+# both run, measured on the B200 pool (profiles/r2/host_zero_vs_d2h.log: 57 and
+# 78 GB/s alone, 110 GB/s together); only their ratio matters.
+_D2H_GBS = 55.0
+_CLEAR_GBS = 55.0
 
 
 def _zero_planes(plan) -> tuple[frozenset, frozenset]:
@@ -514,6 +519,15 @@ def _download(s: PauliSumSoA, zero_x=frozenset(), zero_z=frozenset(),
 
     W = s.x.shape[0]
     hx, hz, hk, hc = (pinned_like(t) for t in (s.x, s.z, s.flags, s.coeffs))
+    # The DMA engine and the host cores work at the same time, so the
+    # proved-zero planes are split between them: with n_nz plane-equivalents
+    # that must be copied and Z proved-zero planes, copying
+    # (Z*R_d - n_nz*R_c) / (R_c + R_d) of the zero planes too makes both finish
+    # together (R_d, R_c: D2H and host-clear rates while both run).
+    zeros = [(hx, s.x, w) for w in sorted(zero_x)] + [(hz, s.z, w) for w in sorted(zero_z)]
+    n_nz = (2 * W - len(zeros)) + 2.0  # non-zero planes + the coefficients (16 B = two words)
+    n_dma = int(max(0.0, (len(zeros) * _D2H_GBS - n_nz * _CLEAR_GBS) / (_CLEAR_GBS + _D2H_GBS)))
+    by_dma, by_host = zeros[:n_dma], zeros[n_dma:]
     fetch(hc, s.coeffs)
     for h, t, zero in ((hx, s.x, zero_x), (hz, s.z, zero_z)):
         if not zero:
@@ -524,10 +538,11 @@ def _download(s: PauliSumSoA, zero_x=frozenset(), zero_z=frozenset(),
                     fetch(h[w], t[w])
     if not zero_flags:
         fetch(hk, s.flags)
+    for h, t, w in by_dma:  # zero on the device as well: copied like any other plane
+        fetch(h[w], t[w])
     # host-side clears overlap the copies in flight
-    for h, zero in ((hx, zero_x), (hz, zero_z)):
-        for w in sorted(zero):
-            h[w].zero_()
+    for h, _, w in by_host:
+        h[w].zero_()
     if zero_flags:
         hk.zero_()
     torch.cuda.current_stream(s.device).synchronize()
