@@ -545,17 +545,23 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
 }
 
 // ------------------------------------------------------------ update
+// kUpdCtas CTAs; thread t of CTA c takes batch term kUpdCtas * t + c, so the
+// pair_checks loops (u < i) of a CTA's warps have mixed lengths and the O(B^2)
+// count is spread over kUpdCtas SMs (one 1024-thread CTA: 39 us per batch).
+constexpr int kUpdCtas = 8;
+constexpr int kUpdThreads = kGB / kUpdCtas;
+
 template <int W>
-__global__ void __launch_bounds__(kGB, 1) k_group_update(GCtx G, int64_t b0, int bn,
-                                                         const uint32_t* g0_snap) {
+__global__ void __launch_bounds__(kUpdThreads) k_group_update(GCtx G, int64_t b0, int bn,
+                                                              const uint32_t* g0_snap) {
   constexpr int E = 128 * W;
-  __shared__ int32_t sg[kGB];
-  __shared__ unsigned long long red[32];
+  __shared__ __align__(16) int32_t sg[kGB];
+  __shared__ unsigned long long red[kUpdThreads / 32];
   if (*G.overflow) return;
   const uint32_t g0_batch = *g0_snap;  // groups that existed at batch start
-  const int i = threadIdx.x;
-  if (i < bn) sg[i] = G.group_of[b0 + i];
+  for (int u = threadIdx.x; u < bn; u += kUpdThreads) sg[u] = G.group_of[b0 + u];
   __syncthreads();
+  const int i = threadIdx.x * kUpdCtas + blockIdx.x;
   unsigned long long chk = 0;
   if (i < bn) {
     const int s = G.tslot[i];
@@ -568,16 +574,22 @@ __global__ void __launch_bounds__(kGB, 1) k_group_update(GCtx G, int64_t b0, int
     for (uint32_t k = 0; k < cnt; ++k) atomicOr(&T[swap_entry(G.list[off + k], W)], bit);
     // pair_checks: #{u < t : group(u) <= group(t)}
     const int c = sg[i];
-    chk = (uint32_t)c < g0_batch ? (unsigned long long)G.gpre[c] : (unsigned long long)b0;
-    for (int u = 0; u < i; ++u) chk += sg[u] <= c ? 1ull : 0ull;
+    uint32_t cnt_le = 0;
+    int u = 0;
+    for (; u + 4 <= i; u += 4) {  // sg is 16-byte aligned: one 128-bit load per four terms
+      const int4 v = *reinterpret_cast<const int4*>(&sg[u]);
+      cnt_le += (v.x <= c) + (v.y <= c) + (v.z <= c) + (v.w <= c);
+    }
+    for (; u < i; ++u) cnt_le += sg[u] <= c ? 1u : 0u;
+    chk = ((uint32_t)c < g0_batch ? (unsigned long long)G.gpre[c] : (unsigned long long)b0) + cnt_le;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) chk += __shfl_xor_sync(0xffffffffu, chk, o);
-  if ((i & 31) == 0) red[i >> 5] = chk;
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = chk;
   __syncthreads();
-  if (i == 0) {
+  if (threadIdx.x == 0) {
     unsigned long long s = 0;
-    for (int w = 0; w < kGB / 32; ++w) s += red[w];
+    for (int w = 0; w < kUpdThreads / 32; ++w) s += red[w];
     atomicAdd(G.checks, s);
   }
 }
@@ -807,7 +819,7 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
     }
     {
       StageTimer t_(st, "k_group_update");
-      k_group_update<W><<<1, kGB, 0, st>>>(G, b0, bn, g0snap);
+      k_group_update<W><<<kUpdCtas, kUpdThreads, 0, st>>>(G, b0, bn, g0snap);
     }
     PLB_CHECK_LAUNCH("grouping batch");
   }
