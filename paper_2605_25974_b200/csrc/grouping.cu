@@ -122,10 +122,18 @@ __device__ __forceinline__ bool deep_fit_warp(const GCtx& G, int g, const uint16
 constexpr int kFitThreads = 256;
 constexpr int kFitSplitWords = 96;  // below this many 32-group words the split shape runs
 
+__host__ __device__ constexpr int fit_gpc(int W, int threads) {
+  return (W <= 2 && threads == kFitThreads) ? 32 : 8;
+}
+
 template <int W, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_group_fit(GCtx G, int64_t b0, int bn) {
   constexpr int E = 128 * W;
-  constexpr int GPC = 8;  // groups per shared-memory pass (8 KB x W)
+  // groups per shared-memory pass: 8 (8 KB x W); narrow strings in the split
+  // shape stage all 32 groups of the word at once (64 KB at W = 2): one
+  // staging + barrier phase per word instead of four, and 32 independent
+  // loads per entry (config 3: the kernel is a chain of such phases on 92 CTAs)
+  constexpr int GPC = fit_gpc(W, THREADS);
   extern __shared__ u64 S[];  // [GPC][E]
   if (*G.overflow) return;
   const uint32_t G0 = *G.gcur;
@@ -765,10 +773,11 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
     PLB_CHECK_LAUNCH("k_row_fill");
   }
   const size_t fit_smem = (size_t)8 * 128 * W * 8;
+  const size_t fit_smem_split = (size_t)fit_gpc(W, kFitThreads) * 128 * W * 8;
   PLB_CUDA(cudaFuncSetAttribute(k_group_fit<W, kGB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)fit_smem));
   PLB_CUDA(cudaFuncSetAttribute(k_group_fit<W, kFitThreads>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fit_smem));
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fit_smem_split));
   PLB_CUDA(cudaFuncSetAttribute(k_group_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(ResolveSmem)));
   const size_t lists_smem = lists_smem_bytes<(W <= 8 ? W : 8)>();
@@ -805,7 +814,7 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
     if (b0 > 0) {
       StageTimer t_(st, "k_group_fit");
       k_group_fit<W, kFitThreads><<<dim3((unsigned)fit_grid, kGB / kFitThreads), kFitThreads,
-                                    fit_smem, st>>>(G, b0, bn);
+                                    fit_smem_split, st>>>(G, b0, bn);
       k_group_fit<W, kGB><<<fit_grid, kGB, fit_smem, st>>>(G, b0, bn);
     }
     {
