@@ -404,8 +404,18 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
   for (int r = 0; r < kGAW; ++r) nx[r] = r < bn ? G.anti[(int64_t)r * kGAW + lane] : 0u;
 #pragma unroll
   for (int r = 0; r < kGK; ++r) ncl[r] = G.fitk[r * 32 + lane];  // (in bounds: kGB lists)
+#ifdef PLB_RES_PROF
+  long long tp[6] = {0, 0, 0, 0, 0, 0};
+  int nrounds = 0, nhard = 0;
+#define RES_T(k, expr) { const long long t0_ = clock64(); expr; tp[k] += clock64() - t0_; }
+#else
+#define RES_T(k, expr) { expr; }
+#endif
   for (int i0 = 0, j = 0; i0 < bn && !T.ovf; i0 += 32, ++j) {
     const int cnt = bn - i0 < 32 ? bn - i0 : 32;
+#ifdef PLB_RES_PROF
+    const long long ts0 = clock64();
+#endif
 #pragma unroll
     for (int r = 0; r < kGAW; ++r) R.aw[r * kMaskLd + lane] = nx[r];
 #pragma unroll
@@ -429,7 +439,14 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
     const uint32_t arow_j = R.aw[lane * kMaskLd + j] & lt_mask;  // anti with earlier lanes
     unsigned todo = cnt == 32 ? 0xffffffffu : ((1u << cnt) - 1u);  // unsettled lanes
     int ck = 0;                                                    // cursor into the candidate list
+#ifdef PLB_RES_PROF
+    tp[0] += clock64() - ts0;
+#endif
     while (todo && !T.ovf) {
+#ifdef PLB_RES_PROF
+      ++nrounds;
+      const long long tr0 = clock64();
+#endif
       const bool mine = todo >> lane & 1u;
       // 1. first fitting old group not blocked by the committed members
       int cand = -1, cslot = -1;
@@ -444,6 +461,10 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
           }
         }
       }
+#ifdef PLB_RES_PROF
+      const long long tr1 = clock64();
+      tp[1] += tr1 - tr0;
+#endif
       // 2. void picks: an earlier unsettled lane took the same group and anti-commutes
       const unsigned have = __ballot_sync(0xffffffffu, mine && cand >= 0);
       bool bad = mine && cand < 0;
@@ -454,19 +475,44 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
       const unsigned badm = __ballot_sync(0xffffffffu, bad);
       const int first_bad = badm ? __ffs(badm) - 1 : 32;
       const unsigned okm = todo & (first_bad >= 32 ? 0xffffffffu : ((1u << first_bad) - 1u));
+#ifdef PLB_RES_PROF
+      const long long tr2 = clock64();
+      tp[2] += tr2 - tr1;
+#endif
       // 3. commit the lanes before the first void one
       if (okm) {
         const bool done = okm >> lane & 1u;
-        unsigned need = __ballot_sync(0xffffffffu, done && cslot < 0);
-        while (need) {  // slots for groups first touched in this batch
-          const int c0 = __shfl_sync(0xffffffffu, cand, __ffs(need) - 1);
-          const int s = new_slot(R, T, c0, -1);
-          if (done && cslot < 0 && cand == c0) cslot = s;
-          need = __ballot_sync(0xffffffffu, done && cslot < 0);
+        // slots for the groups first touched in this batch, all at once: the
+        // lowest lane of every distinct group takes the next slot number,
+        // enters it in the hash table (lock-free: atomicCAS on the key) and
+        // hands it to its peers; the BLOCKED rows are cleared by the whole warp
+        const bool needs = done && cslot < 0;
+        const unsigned need = __ballot_sync(0xffffffffu, needs);
+        if (need) {
+          unsigned peers = 0;
+          if (needs) peers = __match_any_sync(need, cand);
+          const bool leader = needs && (peers & lt_mask) == 0u;
+          const unsigned leaders = __ballot_sync(0xffffffffu, leader);
+          const int base_slot = T.nslots;
+          int s_new = base_slot + __popc(leaders & lt_mask);
+          if (leader) {
+            R.slot_group[s_new] = cand;
+            R.slot_old[s_new] = -1;  // pre-existing group: size loaded after the replay
+            R.slot_cnt[s_new] = 0;
+            int h = (int)(((unsigned)cand * 2654435761u) >> 21) & (kHash - 1);
+            while (atomicCAS(&R.hkey[h], -1, cand) != -1) h = (h + 1) & (kHash - 1);
+            R.hval[h] = s_new;
+          }
+          if (needs) cslot = __shfl_sync(need, s_new, __ffs(peers) - 1);
+          const int n_new = __popc(leaders);
+          for (int k = 0; k < n_new; ++k) R.blocked[(base_slot + k) * kMaskLd + lane] = 0u;
+          T.nslots = base_slot + n_new;
+          __syncwarp();
         }
+        int before = -1;  // rank among the lanes committed to the same slot
         if (done) {
           const unsigned peers = __match_any_sync(okm, cslot);
-          const int before = __popc(peers & lt_mask);
+          before = __popc(peers & lt_mask);
           const int base = R.slot_cnt[cslot];
           __syncwarp(okm);
           if (before == 0) R.slot_cnt[cslot] = base + __popc(peers);
@@ -476,18 +522,30 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
           G.tslot[i] = cslot;
         }
         __syncwarp();
-        if (done) {  // BLOCKED[slot] |= the member's anti row (words < j: terms already settled)
-          uint32_t* brow = R.blocked + cslot * kMaskLd;
-          const uint32_t* arow = R.aw + lane * kMaskLd;
-#pragma unroll 4
-          for (int w = j; w < kGAW; ++w) {  // independent atomics: the loop pipelines
-            const uint32_t v = arow[w];
-            if (v) atomicOr(&brow[w], v);
+#ifdef PLB_RES_PROF
+        const long long tc1 = clock64();
+        tp[5] += tc1 - tr2;
+#endif
+        // BLOCKED[slot] |= the member's anti row (words < j: terms already
+        // settled).  Plain read-modify-writes, one lane per slot at a time
+        // (pass r = the lanes of rank r in their slot; usually one or two
+        // passes): shared-memory atomics cost ~85 cycles each here and do not
+        // pipeline (168k of a batch's 470k cycles on config 3).
+        for (int r = 0; __any_sync(0xffffffffu, before >= r); ++r) {
+          if (before == r) {
+            uint32_t* brow = R.blocked + cslot * kMaskLd;
+            const uint32_t* arow = R.aw + lane * kMaskLd;
+#pragma unroll 8
+            for (int w = j; w < kGAW; ++w) brow[w] |= arow[w];
           }
+          __syncwarp();
         }
-        __syncwarp();
         todo &= ~okm;
       }
+#ifdef PLB_RES_PROF
+      const long long tr3 = clock64();
+      tp[3] += tr3 - tr2;
+#endif
       if (first_bad < 32) {
         const bool hard = __shfl_sync(0xffffffffu, (int)(cand < 0), first_bad) != 0;
         if (hard) {
@@ -497,9 +555,20 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
           todo &= ~(1u << first_bad);
         }
         // a void pick is blocked by the commit above: its cursor moves on next round
+#ifdef PLB_RES_PROF
+        if (hard) ++nhard;
+#endif
       }
+#ifdef PLB_RES_PROF
+      tp[4] += clock64() - tr3;
+#endif
     }
   }
+#ifdef PLB_RES_PROF
+  if (lane == 0 && (b0 == 51200 || b0 == 10240))
+    printf("RESPROF b0=%lld stage=%lld cursor=%lld vote=%lld commit=%lld (pre-blocked %lld) hard=%lld rounds=%d nhard=%d nslots=%d nnew=%d\n",
+           (long long)b0, tp[0], tp[1], tp[2], tp[3], tp[5], tp[4], nrounds, nhard, T.nslots, T.nnew);
+#endif
   if (T.ovf) {
     if (lane == 0) *G.overflow = 1;
     return;
