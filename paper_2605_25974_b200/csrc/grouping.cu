@@ -509,10 +509,9 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
           T.nslots = base_slot + n_new;
           __syncwarp();
         }
-        int before = -1;  // rank among the lanes committed to the same slot
         if (done) {
           const unsigned peers = __match_any_sync(okm, cslot);
-          before = __popc(peers & lt_mask);
+          const int before = __popc(peers & lt_mask);
           const int base = R.slot_cnt[cslot];
           __syncwarp(okm);
           if (before == 0) R.slot_cnt[cslot] = base + __popc(peers);
@@ -526,20 +525,31 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
         const long long tc1 = clock64();
         tp[5] += tc1 - tr2;
 #endif
-        // BLOCKED[slot] |= the member's anti row (words < j: terms already
-        // settled).  Plain read-modify-writes, one lane per slot at a time
-        // (pass r = the lanes of rank r in their slot; usually one or two
-        // passes): shared-memory atomics cost ~85 cycles each here and do not
-        // pipeline (168k of a batch's 470k cycles on config 3).
-        for (int r = 0; __any_sync(0xffffffffu, before >= r); ++r) {
-          if (before == r) {
-            uint32_t* brow = R.blocked + cslot * kMaskLd;
-            const uint32_t* arow = R.aw + lane * kMaskLd;
-#pragma unroll 8
-            for (int w = j; w < kGAW; ++w) brow[w] |= arow[w];
+        // BLOCKED[slot] |= the member's anti row, lane = word: one committed
+        // term per step, its row and slot fetched two steps ahead (the rows
+        // never alias BLOCKED; the read-modify-writes of one slot stay in
+        // order).  Shared-memory atomics (lane = term, loop over words) cost
+        // ~85 cycles each here and do not pipeline: 168k of a batch's 470k
+        // cycles on config 3; rank-ordered plain passes 123k.
+        {
+          unsigned m = okm;
+          int l_a = m ? __ffs(m) - 1 : 0;
+          m &= m - 1;
+          int s_a = __shfl_sync(0xffffffffu, cslot, l_a);
+          uint32_t v_a = R.aw[l_a * kMaskLd + lane];
+          for (;;) {
+            const bool more = m != 0u;
+            const int l_b = more ? __ffs(m) - 1 : 0;
+            m &= m - 1;
+            const int s_b = __shfl_sync(0xffffffffu, cslot, l_b);
+            const uint32_t v_b = R.aw[l_b * kMaskLd + lane];
+            R.blocked[s_a * kMaskLd + lane] |= v_a;
+            if (!more) break;
+            s_a = s_b;
+            v_a = v_b;
           }
-          __syncwarp();
         }
+        __syncwarp();
         todo &= ~okm;
       }
 #ifdef PLB_RES_PROF
