@@ -254,10 +254,13 @@ __global__ void __launch_bounds__(1024) k_group_firstk(GCtx G, int bn) {
 //      or if it has no old group left ("hard");
 //   3. the lanes before the first void one are committed together (slots,
 //      member ranks, BLOCKED |= their anti rows).  A void pick becomes blocked
-//      by that commit, so its cursor moves on in the next round; a hard lane
-//      is settled alone: the rest of its fit0 row from global memory (when it
-//      fits more than kGK old groups), then the groups opened in this batch,
-//      32 per step (one bit test per lane), else a new group.
+//      by that commit, so its cursor moves on in the next round.  Hard lanes
+//      are settled alone: one whose list was complete can only join a group
+//      opened in this batch (32 tested per step, one bit test per lane) or
+//      open one -- lanes with an old candidate never pick those groups, so
+//      such lanes do not end the round and are settled, in order, right after
+//      the commit; one that fits more than kGK old groups ends the round and
+//      walks the rest of its fit0 row from global memory first.
 // Blocked bits only ever get set, so cursors never move back; the outcome is
 // exactly the sequential first-fit.
 constexpr int kMaskLd = kGAW + 1;  // padded rows: lanes reading one word of 32 rows hit 32 banks
@@ -466,15 +469,22 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
       tp[1] += tr1 - tr0;
 #endif
       // 2. void picks: an earlier unsettled lane took the same group and anti-commutes
+      // A lane with no old group left and a complete list can only go to a
+      // group opened inside this batch; such groups are never chosen by lanes
+      // that still have an old candidate, so it does not end the round: it is
+      // deferred and settled (in lane order) after this round's commit.
       const unsigned have = __ballot_sync(0xffffffffu, mine && cand >= 0);
-      bool bad = mine && cand < 0;
+      const bool deferred = mine && cand < 0 && nf <= kGK;
+      bool bad = mine && cand < 0 && nf > kGK;  // the rest of its fit0 row holds old groups
       if (mine && cand >= 0) {
         const unsigned peers = __match_any_sync(have, cand);
         bad = (arow_j & peers) != 0u;
       }
       const unsigned badm = __ballot_sync(0xffffffffu, bad);
       const int first_bad = badm ? __ffs(badm) - 1 : 32;
-      const unsigned okm = todo & (first_bad >= 32 ? 0xffffffffu : ((1u << first_bad) - 1u));
+      const unsigned before_bad = first_bad >= 32 ? 0xffffffffu : ((1u << first_bad) - 1u);
+      const unsigned okm = have & before_bad;
+      const unsigned defm = __ballot_sync(0xffffffffu, deferred) & before_bad;
 #ifdef PLB_RES_PROF
       const long long tr2 = clock64();
       tp[2] += tr2 - tr1;
@@ -525,28 +535,28 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
         const long long tc1 = clock64();
         tp[5] += tc1 - tr2;
 #endif
-        // BLOCKED[slot] |= the member's anti row, lane = word: one committed
-        // term per step, its row and slot fetched two steps ahead (the rows
-        // never alias BLOCKED; the read-modify-writes of one slot stay in
-        // order).  Shared-memory atomics (lane = term, loop over words) cost
-        // ~85 cycles each here and do not pipeline: 168k of a batch's 470k
-        // cycles on config 3; rank-ordered plain passes 123k.
-        {
-          unsigned m = okm;
-          int l_a = m ? __ffs(m) - 1 : 0;
+        // BLOCKED[slot] |= the member's anti row, lane = word, two committed
+        // terms per step (their read-modify-writes are independent unless they
+        // share the slot).  Shared-memory atomics (lane = term, loop over
+        // words) cost ~85 cycles each here and do not pipeline: 168k of a
+        // batch's 470k cycles on config 3; one term per step 114k.
+        for (unsigned m = okm; m;) {  // two committed terms per step
+          const int l_a = __ffs(m) - 1;
           m &= m - 1;
-          int s_a = __shfl_sync(0xffffffffu, cslot, l_a);
-          uint32_t v_a = R.aw[l_a * kMaskLd + lane];
-          for (;;) {
-            const bool more = m != 0u;
-            const int l_b = more ? __ffs(m) - 1 : 0;
-            m &= m - 1;
-            const int s_b = __shfl_sync(0xffffffffu, cslot, l_b);
-            const uint32_t v_b = R.aw[l_b * kMaskLd + lane];
-            R.blocked[s_a * kMaskLd + lane] |= v_a;
-            if (!more) break;
-            s_a = s_b;
-            v_a = v_b;
+          const bool two = m != 0u;
+          const int l_b = two ? __ffs(m) - 1 : l_a;
+          m &= m - 1;
+          const int s_a = __shfl_sync(0xffffffffu, cslot, l_a);
+          const int s_b = __shfl_sync(0xffffffffu, cslot, l_b);
+          const uint32_t v_a = R.aw[l_a * kMaskLd + lane];
+          const uint32_t v_b = two ? R.aw[l_b * kMaskLd + lane] : 0u;
+          const uint32_t o_a = R.blocked[s_a * kMaskLd + lane];
+          const uint32_t o_b = R.blocked[s_b * kMaskLd + lane];
+          if (s_a == s_b) {
+            R.blocked[s_a * kMaskLd + lane] = o_a | v_a | v_b;
+          } else {
+            R.blocked[s_a * kMaskLd + lane] = o_a | v_a;
+            R.blocked[s_b * kMaskLd + lane] = o_b | v_b;
           }
         }
         __syncwarp();
@@ -556,11 +566,17 @@ __global__ void __launch_bounds__(32, 1) k_group_resolve(GCtx G, int64_t b0, int
       const long long tr3 = clock64();
       tp[3] += tr3 - tr2;
 #endif
-      if (first_bad < 32) {
+      for (unsigned m = defm; m && !T.ovf; m &= m - 1) {  // deferred lanes, in order
+        resolve_hard(G, R, T, b0, i0 + __ffs(m) - 1, nwords, -1);
+#ifdef PLB_RES_PROF
+        ++nhard;
+#endif
+      }
+      todo &= ~defm;
+      if (first_bad < 32 && !T.ovf) {
         const bool hard = __shfl_sync(0xffffffffu, (int)(cand < 0), first_bad) != 0;
-        if (hard) {
-          const int nfb = __shfl_sync(0xffffffffu, nf, first_bad);
-          const int last = nfb > kGK ? R.cl[first_bad * (kGK + 1) + kGK - 1] : -1;
+        if (hard) {  // listed candidates exhausted, more old groups in the fit0 row
+          const int last = R.cl[first_bad * (kGK + 1) + kGK - 1];
           resolve_hard(G, R, T, b0, i0 + first_bad, nwords, last);
           todo &= ~(1u << first_bad);
         }
