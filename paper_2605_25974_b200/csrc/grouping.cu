@@ -114,12 +114,13 @@ __device__ __forceinline__ bool deep_fit_warp(const GCtx& G, int g, const uint16
 }
 
 // Two launch shapes, chosen on the device by the group count (the host never
-// reads it): THREADS = kGB, one CTA per 32 groups with every batch term (the
-// staged group chunks are shared by 1024 terms: best with many groups), or
-// THREADS = kFitThreads with blockIdx.y = term block (4x the CTAs: a few
-// hundred groups -- config 3: 23 words -- still fill the SMs).  Each launch
-// returns at once when the other shape applies.
+// reads it): kFitBigThreads terms per CTA, one CTA per (32 groups, half of the
+// batch) -- the staged group chunks are shared by 512 terms and three 64 KB
+// CTAs fit an SM at W = 8 -- or kFitThreads-term blocks (4x the CTAs again: a
+// few hundred groups -- config 3: 23 words -- still fill the SMs).  Each
+// launch returns at once when the other shape applies.
 constexpr int kFitThreads = 256;
+constexpr int kFitBigThreads = 512;  // many groups: half the batch per CTA (three 64 KB CTAs per SM at W = 8)
 constexpr int kFitSplitWords = 96;  // below this many 32-group words the split shape runs
 
 __host__ __device__ constexpr int fit_gpc(int W, int threads) {
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(THREADS) k_group_fit(GCtx G, int64_t b0, int b
   extern __shared__ u64 S[];  // [GPC][E]
   if (*G.overflow) return;
   const uint32_t G0 = *G.gcur;
-  if ((THREADS == kGB) == (((int64_t)G0 + 31) / 32 < kFitSplitWords)) return;
+  if ((THREADS == kFitBigThreads) == (((int64_t)G0 + 31) / 32 < kFitSplitWords)) return;
   const int t = blockIdx.y * THREADS + threadIdx.x;
   const bool valid = t < bn;
   uint32_t off = 0, cnt = 0;
@@ -869,7 +870,7 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
   }
   const size_t fit_smem = (size_t)8 * 128 * W * 8;
   const size_t fit_smem_split = (size_t)fit_gpc(W, kFitThreads) * 128 * W * 8;
-  PLB_CUDA(cudaFuncSetAttribute(k_group_fit<W, kGB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  PLB_CUDA(cudaFuncSetAttribute(k_group_fit<W, kFitBigThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)fit_smem));
   PLB_CUDA(cudaFuncSetAttribute(k_group_fit<W, kFitThreads>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fit_smem_split));
@@ -910,7 +911,8 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
       StageTimer t_(st, "k_group_fit");
       k_group_fit<W, kFitThreads><<<dim3((unsigned)fit_grid, kGB / kFitThreads), kFitThreads,
                                     fit_smem_split, st>>>(G, b0, bn);
-      k_group_fit<W, kGB><<<fit_grid, kGB, fit_smem, st>>>(G, b0, bn);
+      k_group_fit<W, kFitBigThreads><<<dim3((unsigned)fit_grid, kGB / kFitBigThreads),
+                                       kFitBigThreads, fit_smem, st>>>(G, b0, bn);
     }
     {
       StageTimer t_(st, "k_group_firstk");
