@@ -140,3 +140,10 @@ def test_c5_grouping_full_and_prefix(cuda):
     assert np.array_equal(gfull[:pre], gof_ref)
     assert int(full[1].item()) == int(gfull.max()) + 1
     assert int(full[2].item()) == R.pair_checks_from_assignment(gfull)
+    # first-fit is prefix-closed: a 300,000-term prefix (2,269 groups, 2.9e10
+    # reference pair checks, ~15 s of the C oracle) against the full run.  The
+    # whole 10^6-term run was compared once with tools/gpu/check_c5_group_prefix.py.
+    long_pre = 300_000
+    gof_long, ng_long, _ = cgreedy.greedy(x[:long_pre], z[:long_pre])
+    assert np.array_equal(gfull[:long_pre], np.asarray(gof_long))
+    assert int(gfull[:long_pre].max()) + 1 == ng_long
