@@ -35,6 +35,7 @@
 // the bucket structure, CTA schedule or GPU count.
 #pragma once
 #include <algorithm>
+#include <climits>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -218,27 +219,30 @@ __device__ __forceinline__ void pack_key(const Layout& L, const u64 (&zc)[W], co
   }
 }
 
-// Plane word q of a sparse key staged at KS[d * T + e], consuming the slots
-// from cursor k on (planes are visited in order, so every slot whose position
-// precedes plane q's range was consumed by an earlier plane).
+// Packed position of slot k of the sparse key staged at KS[d * T + e]
+// (INT_MAX past the last slot / at the terminator).
+__device__ __forceinline__ int sparse_slot_pos(const Layout& L, const u64* KS, int T, int e, int k) {
+  if (k >= L.nslots) return INT_MAX;
+  const int bit = k * L.sbits, wi = bit >> 6, off = bit & 63;
+  const u64 a = KS[wi * T + e];
+  const u64 b = off + L.sbits > 64 ? KS[(wi + 1) * T + e] : 0ull;
+  const u64 hiw = off ? ((a << off) | (b >> (64 - off))) : a;
+  const u64 v = hiw >> (64 - L.sbits);
+  return v == 0 ? INT_MAX : L.key_bits - (int)v;
+}
+
+// Plane word q of a sparse key, consuming the slots from cursor k on (planes
+// are visited in order, so every slot whose position precedes plane q's range
+// was consumed by an earlier plane).  p is the decoded position of slot k:
+// a slot is decoded once, not once per plane it is compared with.
 __device__ __forceinline__ u64 sparse_plane_next(const Layout& L, const u64* KS, int T, int e,
-                                                 int q, int& k) {
+                                                 int q, int& k, int& p) {
   const int len = L.len[q];
   const int lo = L.pos[q], hi = L.pos[q] + len;
   u64 w = 0;
-  for (; k < L.nslots; ++k) {
-    const int bit = k * L.sbits, wi = bit >> 6, off = bit & 63;
-    const u64 a = KS[wi * T + e];
-    const u64 b = off + L.sbits > 64 ? KS[(wi + 1) * T + e] : 0ull;
-    const u64 hiw = off ? ((a << off) | (b >> (64 - off))) : a;
-    const u64 v = hiw >> (64 - L.sbits);
-    if (v == 0) {
-      k = L.nslots;
-      break;
-    }
-    const int p = L.key_bits - (int)v;
-    if (p >= hi) break;
+  while (p < hi) {
     w |= 1ull << (L.lo[q] + len - 1 - (p - lo));
+    p = sparse_slot_pos(L, KS, T, e, ++k);
   }
   return w;
 }
@@ -709,7 +713,7 @@ __device__ __forceinline__ void pack_sparse(const Layout& L, const u64 (&seg)[2 
 }
 
 template <int W, int KW, int MODE>
-__global__ void __launch_bounds__(256) k_pack_ops(Layout L, SrcA S, int64_t ma, int64_t mb, Ctl C) {
+__global__ void __launch_bounds__(256, 4) k_pack_ops(Layout L, SrcA S, int64_t ma, int64_t mb, Ctl C) {
   const int64_t n = ma + (MODE == 0 ? mb : 0);
   if constexpr (MODE == 1 && W <= 8) if (L.sparse) {
     for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x; t0 < n; t0 += (int64_t)gridDim.x * blockDim.x) {

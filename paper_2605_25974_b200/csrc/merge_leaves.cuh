@@ -935,9 +935,12 @@ k_emit(Layout L, Dims D, Ctl C, OutP O) {
     // plane-major stores: each plane gets T*8 contiguous bytes from this CTA
     // (sparse keys: the slots are sorted by packed position and the planes
     // cover ascending position ranges, so one cursor per term walks them once)
-    int cur[PER];
+    int cur[PER], curp[PER];  // sparse keys: slot cursor and its decoded position
 #pragma unroll
-    for (int u = 0; u < PER; ++u) cur[u] = 0;
+    for (int u = 0; u < PER; ++u) {
+      cur[u] = 0;
+      curp[u] = L.sparse ? sparse_slot_pos(L, KS, T, u * kEmitThreads + tid, 0) : 0;
+    }
     for (int q = 0; q < 2 * W; ++q) {
       const int len = L.len[q];
       u64* dst = (q < W ? O.oz + (int64_t)q * O.ldo : O.ox + (int64_t)(q - W) * O.ldo) + o0;
@@ -954,7 +957,7 @@ k_emit(Layout L, Dims D, Ctl C, OutP O) {
         if ((uint32_t)o0 + e >= o1) break;
         u64 w = 0;
         if (L.sparse) {
-          if (len) w = sparse_plane_next(L, KS, T, e, q, cur[u]);
+          if (len) w = sparse_plane_next(L, KS, T, e, q, cur[u], curp[u]);
         } else if (len) {
           const u64 a = KS[wi * T + e];
           const u64 b = (off && wi + 1 < KW) ? KS[(wi + 1) * T + e] : 0ull;
