@@ -184,7 +184,7 @@ static int run_merge(int64_t M, const u64* x, const u64* z, int64_t ld, const in
     PLB_CUDA(cudaMemsetAsync(cross, 0, (size_t)kMergeBatch * kMergeBatch + (size_t)kMergeBatch * gstride, st));
     k_merge_anti<W><<<grid, kMergeThreads, 0, st>>>(x, z, ld, M, gid, lg, members, local_off[l0],
                                                     local_off[l1], l0, bad, gstride, cross);
-    k_merge_pick<<<1, 1024, 0, st>>>(gid, lg, members, loff, l0, l1, bad, gstride, cross, gsize,
+    k_merge_pick<<<1, 256, 0, st>>>(gid, lg, members, loff, l0, l1, bad, gstride, cross, gsize,
                                       n_global, global_of_local, pair_checks);
   }
   PLB_CHECK_LAUNCH("k_group_merge");
