@@ -153,15 +153,23 @@ __global__ void __launch_bounds__(THREADS) k_group_fit(GCtx G, int64_t b0, int b
 #pragma unroll 1
     for (int h = 0; h < 32 / GPC; ++h) {
       const int64_t g0 = gw * 32 + h * GPC;
-      for (int i = threadIdx.x; i < GPC * E; i += blockDim.x) {
-        const int gi = i / E, e = i % E;
-        const int64_t g = g0 + gi;
-        u64 v = 0;
-        if (g < G0) {
-          const int c = G.gfirst[g];
-          v = G.pool[(int64_t)c * E + e];
+      // staging: eight (chunk pointer -> chunk word) load pairs in flight per
+      // thread (a rolled loop issued them one pair at a time: a chain of 16
+      // dependent HBM round trips per pass on config 5)
+      static_assert((GPC * E) % (THREADS * 8) == 0 || GPC * E < THREADS * 8, "staging tiles");
+      constexpr int kStageIter = GPC * E / THREADS;
+      constexpr int kStageBatch = kStageIter < 8 ? kStageIter : 8;
+#pragma unroll 1
+      for (int it0 = 0; it0 < kStageIter; it0 += kStageBatch) {
+        u64 v[kStageBatch];
+#pragma unroll
+        for (int u = 0; u < kStageBatch; ++u) {
+          const int i = threadIdx.x + (it0 + u) * THREADS;
+          const int64_t g = g0 + i / E;
+          v[u] = g < G0 ? G.pool[(int64_t)G.gfirst[g] * E + i % E] : 0ull;
         }
-        S[gi * E + e] = v;
+#pragma unroll
+        for (int u = 0; u < kStageBatch; ++u) S[threadIdx.x + (it0 + u) * THREADS] = v[u];
       }
       __syncthreads();
       uint32_t cand = 0;  // staged groups whose first chunk commutes with the term
