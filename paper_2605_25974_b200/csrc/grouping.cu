@@ -65,6 +65,11 @@ struct GCtx {
   int32_t* gtb_last;                   // gcap
   int64_t tcap;
   uint32_t* tb_pool_next;
+  // deep-fit queue: (batch term, group) pairs whose first chunk commutes and
+  // whose group has more chunks, finished by k_group_deepfit with every warp
+  uint2* dq;
+  uint32_t* dq_count;
+  uint32_t dq_cap;
   // scalars
   uint32_t* gcur;                      // groups so far
   uint32_t* pool_next;
@@ -119,6 +124,7 @@ __device__ __forceinline__ bool deep_fit_warp(const GCtx& G, int g, const uint16
 // CTAs fit an SM at W = 8 -- or kFitThreads-term blocks (4x the CTAs again: a
 // few hundred groups -- config 3: 23 words -- still fill the SMs).  Each
 // launch returns at once when the other shape applies.
+constexpr uint32_t kDeepQueue = 1u << 20;  // deep-fit pairs queued per batch (the rest run inline)
 constexpr int kFitThreads = 256;
 constexpr int kFitBigThreads = 512;  // many groups: half the batch per CTA (three 64 KB CTAs per SM at W = 8)
 constexpr int kFitSplitWords = 96;  // below this many 32-group words the split shape runs
@@ -184,15 +190,21 @@ __global__ void __launch_bounds__(THREADS) k_group_fit(GCtx G, int64_t b0, int b
         }
 #pragma unroll
         for (int q = 0; q < GPC; ++q) cand |= (acc[q] == 0 && g0 + q < G0 ? 1u : 0u) << q;
-        for (uint32_t cb = cand; cb; cb &= cb - 1) {  // one-chunk groups are settled
+        for (uint32_t cb = cand; cb; cb &= cb - 1) {
           const int q = __ffs(cb) - 1;
-          if (G.gsize[g0 + q] <= 64) {
+          if (G.gsize[g0 + q] <= 64) {  // one-chunk groups are settled
             word |= 1u << (h * GPC + q);
             cand &= ~(1u << q);
+          } else {  // the rest of the group's chunks: queued for k_group_deepfit
+            const uint32_t slot = atomicAdd(G.dq_count, 1u);
+            if (slot < G.dq_cap) {
+              G.dq[slot] = make_uint2((uint32_t)t, (uint32_t)(g0 + q));
+              cand &= ~(1u << q);
+            }
           }
         }
       }
-      // larger groups: the warp takes the (term, group) pairs one at a time
+      // (queue full: the warp finishes the remaining pairs itself, one at a time)
       for (unsigned pend = __ballot_sync(0xffffffffu, cand != 0u); pend;
            pend = __ballot_sync(0xffffffffu, cand != 0u)) {
         const int L = __ffs(pend) - 1;
@@ -209,6 +221,26 @@ __global__ void __launch_bounds__(THREADS) k_group_fit(GCtx G, int64_t b0, int b
       __syncthreads();
     }
     if (valid) G.fit0[(int64_t)t * G.gw_stride + gw] = word;
+  }
+}
+
+// Deep fits of the queued (term, group) pairs, one pair per warp at a time over
+// the whole GPU; a fitting pair sets its bit in the term's fit0 row.  Inside
+// k_group_fit the pairs ran between the CTA's barriers on whichever warp owned
+// the term: the groups with many chunks sit in the first words, so a few CTAs
+// carried most of them.
+template <int W>
+__global__ void __launch_bounds__(256) k_group_deepfit(GCtx G, int64_t b0) {
+  if (*G.overflow) return;
+  const uint32_t n = min(*G.dq_count, G.dq_cap);
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nwarps) {
+    const uint2 pr = G.dq[i];
+    const uint32_t off = G.off[b0 + pr.x], cnt = G.off[b0 + pr.x + 1] - off;
+    const int g = (int)pr.y;
+    if (deep_fit_warp<W>(G, g, G.list + off, cnt, (int)((G.gsize[g] + 63) / 64)) &&
+        (threadIdx.x & 31) == 0)
+      atomicOr(&G.fit0[(int64_t)pr.x * G.gw_stride + (g >> 5)], 1u << (g & 31));
   }
 }
 
@@ -782,6 +814,7 @@ static int64_t fixed_bytes(int W, int64_t M) {
   o += a256((int64_t)kGB * kGK * 4) + a256(kGB * 4) + a256((int64_t)kAntiSuper * kGB * kGAW * 4);
   o += a256(kGB * 4) * 3 + a256((int64_t)kGB * kSlotChunks * 4);
   o += a256(16);                                // g0 snapshot
+  o += a256((int64_t)kDeepQueue * 8);           // deep-fit queue
   return o;
 }
 
@@ -814,6 +847,8 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
   G.slot_old = (int32_t*)take(kGB * 4);
   G.slot_chunks = (int32_t*)take((int64_t)kGB * kSlotChunks * 4);
   uint32_t* g0snap = (uint32_t*)take(16);
+  G.dq_cap = kDeepQueue;
+  G.dq = (uint2*)take((int64_t)kDeepQueue * 8);
   if (o > (int64_t)ws_bytes) {
     set_error("pl_group_greedy: workspace too small");
     return PL_ERR_WORKSPACE;
@@ -823,6 +858,7 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
   G.pool_next = scal + 1;
   G.overflow = scal + 2;
   G.tb_pool_next = scal + 8;
+  G.dq_count = scal + 9;
   G.checks = (unsigned long long*)(scal + 4);
   // CSR entry lists of every term (same encoding as the bitmatrix)
   const unsigned nb = (unsigned)ceil_div(M, 256);
@@ -916,11 +952,13 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
       }
     }
     if (b0 > 0) {
+      PLB_CUDA(cudaMemsetAsync(G.dq_count, 0, 4, st));
       StageTimer t_(st, "k_group_fit");
       k_group_fit<W, kFitThreads><<<dim3((unsigned)fit_grid, kGB / kFitThreads), kFitThreads,
                                     fit_smem_split, st>>>(G, b0, bn);
       k_group_fit<W, kFitBigThreads><<<dim3((unsigned)fit_grid, kGB / kFitBigThreads),
                                        kFitBigThreads, fit_smem, st>>>(G, b0, bn);
+      k_group_deepfit<W><<<4 * num_sms(), 256, 0, st>>>(G, b0);
     }
     {
       StageTimer t_(st, "k_group_firstk");
