@@ -479,11 +479,6 @@ def _remember(plan) -> None:
 
 
 LAST_D2H_BYTES = 0  # instrumentation: bytes the most recent _download copied from the device
-# Rates (GB/s) of a pinned D2H copy and of a host clear of pinned memory while
-# both run, measured on the B200 pool (profiles/r2/host_zero_vs_d2h.log: 57 and
-# 78 GB/s alone, 110 GB/s together); only their ratio matters.
-_D2H_GBS = 55.0
-_CLEAR_GBS = 55.0
 
 
 def _zero_planes(plan) -> tuple[frozenset, frozenset]:
@@ -503,9 +498,9 @@ def _download(s: PauliSumSoA, zero_x=frozenset(), zero_z=frozenset(),
     host allocator recycles them): asynchronous copies, then one sync.
 
     Planes the caller proves zero (``_zero_planes``; the phase bytes of a
-    combined sum) are not read over PCIe: they are cleared on the host while
-    the DMA of the other arrays runs (n=500 sums on 48 qubits: 14 of the 16
-    planes)."""
+    combined sum) need not cross PCIe: the host clears them while the DMA of
+    the other arrays runs, and hands some of them to the DMA engine when it
+    runs dry (n=500 sums on 48 qubits: 14 of the 16 planes are zero)."""
     global LAST_D2H_BYTES
     copied = 0
 
@@ -520,14 +515,22 @@ def _download(s: PauliSumSoA, zero_x=frozenset(), zero_z=frozenset(),
     W = s.x.shape[0]
     hx, hz, hk, hc = (pinned_like(t) for t in (s.x, s.z, s.flags, s.coeffs))
     # The DMA engine and the host cores work at the same time, so the
-    # proved-zero planes are split between them: with n_nz plane-equivalents
-    # that must be copied and Z proved-zero planes, copying
-    # (Z*R_d - n_nz*R_c) / (R_c + R_d) of the zero planes too makes both finish
-    # together (R_d, R_c: D2H and host-clear rates while both run).
-    zeros = [(hx, s.x, w) for w in sorted(zero_x)] + [(hz, s.z, w) for w in sorted(zero_z)]
-    n_nz = (2 * W - len(zeros)) + 2.0  # non-zero planes + the coefficients (16 B = two words)
-    n_dma = int(max(0.0, (len(zeros) * _D2H_GBS - n_nz * _CLEAR_GBS) / (_CLEAR_GBS + _D2H_GBS)))
-    by_dma, by_host = zeros[:n_dma], zeros[n_dma:]
+    # proved-zero planes are shared between them dynamically: the host clears
+    # plane quarters from the back of the list, and whenever fewer than three
+    # copies are outstanding the next one from the front goes to the DMA engine
+    # (it is zero on the device too).  Both finish together whatever their
+    # rates are at the moment (the host's memory bandwidth is shared).
+    m = s.x.shape[1]
+    cuts = [0, m] if m < (1 << 22) else [0, m // 4, m // 2, 3 * (m // 4), m]  # finer tail balance
+    zeros = [(h[w, a:b], t[w, a:b]) for h, t, zs in ((hx, s.x, zero_x), (hz, s.z, zero_z))
+             for w in sorted(zs) for a, b in zip(cuts[:-1], cuts[1:])]
+    stream = torch.cuda.current_stream(s.device)
+
+    def mark():
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        return ev
+
     fetch(hc, s.coeffs)
     for h, t, zero in ((hx, s.x, zero_x), (hz, s.z, zero_z)):
         if not zero:
@@ -538,11 +541,18 @@ def _download(s: PauliSumSoA, zero_x=frozenset(), zero_z=frozenset(),
                     fetch(h[w], t[w])
     if not zero_flags:
         fetch(hk, s.flags)
-    for h, t, w in by_dma:  # zero on the device as well: copied like any other plane
-        fetch(h[w], t[w])
-    # host-side clears overlap the copies in flight
-    for h, _, w in by_host:
-        h[w].zero_()
+    inflight = [mark()]
+    front, back = 0, len(zeros)
+    while front < back:
+        inflight = [ev for ev in inflight if not ev.query()]
+        while len(inflight) < 3 and front < back:
+            h, t = zeros[front]
+            front += 1
+            fetch(h, t)
+            inflight.append(mark())
+        if front < back:
+            back -= 1
+            zeros[back][0].zero_()
     if zero_flags:
         hk.zero_()
     torch.cuda.current_stream(s.device).synchronize()

@@ -195,10 +195,10 @@ def test_host_path_zero_planes_on_dirty_buffers(cuda):
         h = pl.sum_multiply(A, B)
         assert h.device.type == "cpu"
         m = len(h)
-        # x0, z0 and the coefficients, plus the share of the 14 proved-zero
-        # planes left to the DMA engine so that it and the host clears end together
-        n_dma = int((14 * S._D2H_GBS - 4 * S._CLEAR_GBS) / (S._D2H_GBS + S._CLEAR_GBS))
-        assert S.LAST_D2H_BYTES == m * (2 * 8 + 16) + n_dma * 8 * m
+        # x0, z0 and the coefficients, plus however many of the 14 proved-zero
+        # planes the DMA engine took while the host cleared the others
+        extra = S.LAST_D2H_BYTES - m * (2 * 8 + 16)
+        assert 0 <= extra <= 14 * 8 * m
         ref = pl.sum_multiply(A.cuda(), B.cuda()).cpu()
         assert h == ref
         assert not h.x[1:].any() and not h.z[1:].any() and not h.flags.any()
