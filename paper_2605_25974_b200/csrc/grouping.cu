@@ -27,6 +27,7 @@
 //             add each term's reference pair_checks contribution
 //             #{u < t : group(u) <= group(t)}.
 #include <algorithm>
+#include <cstdlib>
 
 #include "bitmatrix_kernels.cuh"
 #include "common.cuh"
@@ -848,6 +849,10 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
   G.slot_chunks = (int32_t*)take((int64_t)kGB * kSlotChunks * 4);
   uint32_t* g0snap = (uint32_t*)take(16);
   G.dq_cap = kDeepQueue;
+  if (const char* e = getenv("PLB_DEEP_QUEUE_CAP")) {  // tests: force the inline deep-fit fallback
+    const long v = atol(e);
+    if (v >= 0 && (unsigned long)v < kDeepQueue) G.dq_cap = (uint32_t)v;
+  }
   G.dq = (uint2*)take((int64_t)kDeepQueue * 8);
   if (o > (int64_t)ws_bytes) {
     set_error("pl_group_greedy: workspace too small");

@@ -127,3 +127,19 @@ def test_group_greedy_parallel_errors(cuda):
     s = pl.PauliSumSoA.from_columns(10, *rng.random_columns(10, 4, 1), device=cuda)
     with pytest.raises(ValueError):
         pl.group_greedy_parallel(s, 0)
+
+
+@pytest.mark.parametrize("cap", ["0", "37"])
+def test_deep_fit_queue_overflow_falls_back_inline(cuda, cap, monkeypatch):
+    """(term, group) pairs that do not fit the deep-fit queue are finished by
+    the owning warp inside k_group_fit: same assignment and pair_checks with an
+    empty or a tiny queue (config 3 prefix: groups of many chunks)."""
+    from oracle import cgreedy
+
+    x, z, f, c = rng.config_columns(3, scale=0.2)
+    gof_ref, ng_ref, pc_ref = cgreedy.greedy(x, z)
+    monkeypatch.setenv("PLB_DEEP_QUEUE_CAP", cap)
+    S = pl.PauliSumSoA.from_columns(100, x, z, f, c, device=cuda)
+    gof, ng, pc = pl.group_assignment(S)
+    assert np.array_equal(gof.cpu().numpy(), np.asarray(gof_ref))
+    assert int(ng.item()) == ng_ref and int(pc.item()) == pc_ref
