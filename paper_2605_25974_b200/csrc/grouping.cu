@@ -958,12 +958,15 @@ static int run_group(int64_t M, const u64* x, const u64* z, int64_t ld, int32_t*
     }
     if (b0 > 0) {
       PLB_CUDA(cudaMemsetAsync(G.dq_count, 0, 4, st));
+      {
       StageTimer t_(st, "k_group_fit");
       k_group_fit<W, kFitThreads><<<dim3((unsigned)fit_grid, kGB / kFitThreads), kFitThreads,
                                     fit_smem_split, st>>>(G, b0, bn);
       k_group_fit<W, kFitBigThreads><<<dim3((unsigned)fit_grid, kGB / kFitBigThreads),
                                        kFitBigThreads, fit_smem, st>>>(G, b0, bn);
-      k_group_deepfit<W><<<4 * num_sms(), 256, 0, st>>>(G, b0);
+      }
+      StageTimer t2_(st, "k_group_deepfit");
+      k_group_deepfit<W><<<8 * num_sms(), 256, 0, st>>>(G, b0);
     }
     {
       StageTimer t_(st, "k_group_firstk");
